@@ -1,0 +1,159 @@
+"""CPU oracle of the IEDS surface build (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this package.  It shares no code with the CUDA path and the CUDA path never
+calls it.  The arithmetic lives in ieds_oracle.c (plain C, fp64 / int64), each function
+citing the PAPER.md passage it follows; this module only marshals numpy arrays.
+
+Outputs use the oracle's own representation: byte images [H][W] of 0/1 and int64
+squared distances with NO_EDGE = -1 for "no edge pixel in the frame".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+NO_EDGE = -1
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ieds_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle with gcc (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            P = ctypes.c_void_p
+            i64, i32, f64 = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+            lib.oracle_accumulate.argtypes = [P, i64, i32, i32, P]
+            lib.oracle_accumulate.restype = i32
+            lib.oracle_denoise.argtypes = [P, i32, i32, i32, P]
+            lib.oracle_fill.argtypes = [P, i32, i32, i32, P]
+            lib.oracle_edt_separable.argtypes = [P, i32, i32, P]
+            lib.oracle_edt_bruteforce.argtypes = [P, i32, i32, P]
+            lib.oracle_surface.argtypes = [P, i64, f64, P]
+            lib.oracle_alpha_from_dsat.argtypes = [f64]
+            lib.oracle_alpha_from_dsat.restype = f64
+            lib.oracle_build_window.argtypes = [P, i64, i32, i32, i32, i32, f64, P, P, P, P, P]
+            lib.oracle_build_window.restype = i32
+            _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _img(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+class OracleRangeError(ValueError):
+    """An event lies outside the W x H frame."""
+
+
+def accumulate(xy, width: int, height: int) -> np.ndarray:
+    xy = np.ascontiguousarray(xy, dtype=np.uint32)
+    E = np.zeros((height, width), np.uint8)
+    st = _load().oracle_accumulate(_ptr(xy), len(xy), width, height, _ptr(E))
+    if st != 0:
+        raise OracleRangeError("event outside the frame")
+    return E
+
+
+def denoise(E, n_d: int) -> np.ndarray:
+    E = _img(E)
+    out = np.empty_like(E)
+    _load().oracle_denoise(_ptr(E), E.shape[1], E.shape[0], n_d, _ptr(out))
+    return out
+
+
+def fill(E_d, n_f: int) -> np.ndarray:
+    E_d = _img(E_d)
+    out = np.empty_like(E_d)
+    _load().oracle_fill(_ptr(E_d), E_d.shape[1], E_d.shape[0], n_f, _ptr(out))
+    return out
+
+
+def edt(E_df) -> np.ndarray:
+    """Exact squared EDT (separable, FH lower envelope); NO_EDGE if the frame is empty."""
+    E_df = _img(E_df)
+    out = np.empty(E_df.shape, np.int64)
+    _load().oracle_edt_separable(_ptr(E_df), E_df.shape[1], E_df.shape[0], _ptr(out))
+    return out
+
+
+def edt_bruteforce(E_df) -> np.ndarray:
+    E_df = _img(E_df)
+    out = np.empty(E_df.shape, np.int64)
+    _load().oracle_edt_bruteforce(_ptr(E_df), E_df.shape[1], E_df.shape[0], _ptr(out))
+    return out
+
+
+def surface(D2, alpha: float) -> np.ndarray:
+    D2 = np.ascontiguousarray(D2, dtype=np.int64)
+    out = np.empty(D2.shape, np.float64)
+    _load().oracle_surface(_ptr(D2), D2.size, float(alpha), _ptr(out))
+    return out
+
+
+def alpha_from_dsat(d_sat: float) -> float:
+    return _load().oracle_alpha_from_dsat(float(d_sat))
+
+
+def build_window(xy, width: int, height: int, n_d: int, n_f: int, alpha: float,
+                 want=("E", "E_d", "E_df", "D2", "S")) -> dict:
+    """accumulate -> Alg. 1 -> Alg. 2 -> EDT -> Eq. (1) for one window."""
+    xy = np.ascontiguousarray(xy, dtype=np.uint32)
+    shp = (height, width)
+    out = {}
+    bufs = {}
+    for k, dt in (("E", np.uint8), ("E_d", np.uint8), ("E_df", np.uint8), ("D2", np.int64), ("S", np.float64)):
+        bufs[k] = np.empty(shp, dt) if k in want else None
+    st = _load().oracle_build_window(
+        _ptr(xy), len(xy), width, height, n_d, n_f, float(alpha),
+        *[(_ptr(bufs[k]) if bufs[k] is not None else None) for k in ("E", "E_d", "E_df", "D2", "S")])
+    if st == -1:
+        raise ValueError("invalid parameters")
+    if st == -2:
+        raise OracleRangeError("event outside the frame")
+    for k in want:
+        out[k] = bufs[k]
+    return out
+
+
+def build_batch(xy, offsets, width: int, height: int, n_d: int, n_f: int, alpha: float,
+                windows=None, threads: int | None = None, want=("S",)) -> list:
+    """Run build_window over windows (list of indices) of a CSR batch on a thread pool.
+
+    ctypes releases the GIL during the C call, so `threads` host cores run concurrently.
+    """
+    xy = np.ascontiguousarray(xy, dtype=np.uint32)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    idx = range(len(offsets) - 1) if windows is None else windows
+    threads = threads or len(os.sched_getaffinity(0))
+
+    def one(i):
+        return build_window(xy[offsets[i]:offsets[i + 1]], width, height, n_d, n_f, alpha, want=want)
+
+    if threads <= 1:
+        return [one(i) for i in idx]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(one, idx))

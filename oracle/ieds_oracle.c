@@ -1,0 +1,259 @@
+/*
+ * ieds_oracle.c -- plain, slow, obviously-correct CPU oracle of the IEDS surface build.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant with the CUDA path (paper_2112_10591_b200/), and the CUDA
+ * path never calls it.
+ *
+ * Source: Brebion, Moreau, Davoine, "Real-Time Optical Flow for Vehicular Perception
+ * with Low- and High-Resolution Event Cameras" (arXiv 2112.10591).  Citations "P:N" are
+ * /root/reference/PAPER.md line numbers; "S:N" are SPEC.md lines.  The readings of
+ * silent / garbled passages are listed in DESIGN.md ("Readings").
+ *
+ * Images are byte images, row-major [H][W], value 0 or 1; pixel (x, y) = column x, row y.
+ * Squared distances are int64; ORACLE_NO_EDGE (-1) marks "no edge pixel in the frame".
+ * Floating point is fp64 throughout.
+ *
+ * Every function is single-threaded and follows the paper's definition step by step.
+ * Parity status: all functions pinned by tests/test_oracle_pins.py (none unpinned).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_NO_EDGE (-1LL)
+#define ORACLE_OK 0
+#define ORACLE_ERANGE (-2)
+#define ORACLE_EINVAL (-1)
+
+/* ---- §III-A Accumulation for edge images -------------------------------
+ * "These binary matrices indicate whether or not each pixel produced at least one event
+ * during the accumulation time"; polarity is not taken into account, so
+ * the oracle takes only the (x, y) coordinates.  Events outside the frame are an error
+ * (S:42); they are not written. */
+int oracle_accumulate(const uint32_t *xy, int64_t n, int W, int H, uint8_t *E)
+{
+    int status = ORACLE_OK;
+    memset(E, 0, (size_t)W * (size_t)H);
+    for (int64_t i = 0; i < n; i++) {
+        int x = (int)(xy[i] & 0xFFFFu);
+        int y = (int)(xy[i] >> 16);
+        if (x >= W || y >= H) {
+            status = ORACLE_ERANGE;
+            continue;
+        }
+        E[(size_t)y * W + x] = 1;
+    }
+    return status;
+}
+
+/* count of edge pixels among the 4 direct neighbour pixels of p in img
+ * (Alg. 1 line "count of edge pixels among the 4 direct neighbour pixels", P:127;
+ *  out-of-frame neighbours count as non-edge: DESIGN.md reading R1) */
+static int count4(const uint8_t *img, int W, int H, int x, int y)
+{
+    int n = 0;
+    if (x > 0 && img[(size_t)y * W + (x - 1)]) n++;
+    if (x + 1 < W && img[(size_t)y * W + (x + 1)]) n++;
+    if (y > 0 && img[(size_t)(y - 1) * W + x]) n++;
+    if (y + 1 < H && img[(size_t)(y + 1) * W + x]) n++;
+    return n;
+}
+
+/* ---- Algorithm 1, Denoising -----------------------------------------------
+ *   E_d <- E
+ *   foreach pixel p in E: if E[p] is an edge pixel:
+ *       n_d <- count of edge pixels among the 4 direct neighbours of p in E
+ *       if n_d < N_d: E_d[p] <- not an edge pixel anymore */
+void oracle_denoise(const uint8_t *E, int W, int H, int N_d, uint8_t *E_d)
+{
+    memcpy(E_d, E, (size_t)W * (size_t)H);
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            if (E[(size_t)y * W + x]) {
+                int n_d = count4(E, W, H, x, y);
+                if (n_d < N_d) E_d[(size_t)y * W + x] = 0;
+            }
+        }
+}
+
+/* ---- Algorithm 2, Filling -------------------------------------------------
+ *   E_df <- E_d
+ *   foreach pixel p in E_d: if E_d[p] is not an edge pixel:
+ *       n_f <- count of edge pixels among the 4 direct neighbours of p in E_d
+ *       if n_f >= N_f: E_df[p] <- becomes an edge pixel
+ * Run strictly after denoising. */
+void oracle_fill(const uint8_t *E_d, int W, int H, int N_f, uint8_t *E_df)
+{
+    memcpy(E_df, E_d, (size_t)W * (size_t)H);
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            if (!E_d[(size_t)y * W + x]) {
+                int n_f = count4(E_d, W, H, x, y);
+                if (n_f >= N_f) E_df[(size_t)y * W + x] = 1;
+            }
+        }
+}
+
+/* ---- §III-C exact Euclidean distance transform --------------------------
+ * d_Euc(p) = Euclidean distance from p to the closest edge pixel of E_df.
+ * The paper uses Coeurjolly et al.'s separable exact EDT.  The oracle uses the
+ * textbook separable form of that family:
+ *   pass 1 (columns): g(x,y) = min |y - y'| over edge pixels (x, y') of column x;
+ *   pass 2 (rows):    D2(x,y) = min_q (x - q)^2 + g(q,y)^2, evaluated with the lower
+ *                     envelope of parabolas (Felzenszwalb & Huttenlocher 2012, "Distance
+ *                     Transforms of Sampled Functions", Algorithm 1 DT(f)), with the
+ *                     parabola intersections in fp64 (exact decisions at these sizes, see
+ *                     DESIGN.md) and the envelope evaluation in int64.
+ * Columns without an edge pixel have g = +inf and contribute no parabola.  If the whole
+ * frame has no edge pixel every D2 is ORACLE_NO_EDGE (reading R5). */
+void oracle_edt_separable(const uint8_t *E_df, int W, int H, int64_t *D2)
+{
+    const int64_t INF = INT64_MAX;
+    int64_t *g = (int64_t *)malloc(sizeof(int64_t) * (size_t)W * (size_t)H);
+    int any = 0;
+    /* pass 1: two sweeps per column */
+    for (int x = 0; x < W; x++) {
+        int64_t last = -1;
+        for (int y = 0; y < H; y++) {
+            if (E_df[(size_t)y * W + x]) last = y;
+            g[(size_t)y * W + x] = (last < 0) ? INF : (int64_t)y - last;
+        }
+        last = -1;
+        for (int y = H - 1; y >= 0; y--) {
+            if (E_df[(size_t)y * W + x]) { last = y; any = 1; }
+            if (last >= 0) {
+                int64_t d = last - (int64_t)y;
+                if (d < g[(size_t)y * W + x]) g[(size_t)y * W + x] = d;
+            }
+        }
+    }
+    if (!any) {
+        for (size_t i = 0; i < (size_t)W * (size_t)H; i++) D2[i] = ORACLE_NO_EDGE;
+        free(g);
+        return;
+    }
+    /* pass 2: FH lower envelope per row over f(q) = g(q,y)^2 */
+    int *v = (int *)malloc(sizeof(int) * (size_t)W);
+    double *z = (double *)malloc(sizeof(double) * (size_t)(W + 1));
+    int64_t *f = (int64_t *)malloc(sizeof(int64_t) * (size_t)W);
+    for (int y = 0; y < H; y++) {
+        for (int q = 0; q < W; q++) {
+            int64_t gq = g[(size_t)y * W + q];
+            f[q] = (gq == INF) ? INF : gq * gq;
+        }
+        int k = -1;
+        for (int q = 0; q < W; q++) {
+            if (f[q] == INF) continue;
+            if (k < 0) {
+                k = 0; v[0] = q; z[0] = -HUGE_VAL; z[1] = HUGE_VAL;
+                continue;
+            }
+            double s;
+            for (;;) {
+                int p = v[k];
+                s = ((double)(f[q] + (int64_t)q * q) - (double)(f[p] + (int64_t)p * p)) /
+                    (2.0 * (double)q - 2.0 * (double)p);
+                if (s <= z[k]) {
+                    k--;
+                    if (k < 0) break;
+                } else
+                    break;
+            }
+            if (k < 0) { /* cannot happen: z[0] = -inf */
+                k = 0; v[0] = q; z[0] = -HUGE_VAL; z[1] = HUGE_VAL;
+                continue;
+            }
+            k++;
+            v[k] = q;
+            z[k] = s;
+            z[k + 1] = HUGE_VAL;
+        }
+        /* every row has a finite parabola because some column has an edge pixel */
+        k = 0;
+        for (int q = 0; q < W; q++) {
+            while (z[k + 1] < (double)q) k++;
+            int64_t d = (int64_t)q - v[k];
+            D2[(size_t)y * W + q] = d * d + f[v[k]];
+        }
+    }
+    free(v); free(z); free(f); free(g);
+}
+
+/* Brute force: D2(p) = min over edge pixels q of |p - q|^2 (definition).
+ * O(W*H*K); for tiny frames only. */
+void oracle_edt_bruteforce(const uint8_t *E_df, int W, int H, int64_t *D2)
+{
+    int64_t nset = 0;
+    for (size_t i = 0; i < (size_t)W * (size_t)H; i++) nset += E_df[i] != 0;
+    int *ex = (int *)malloc(sizeof(int) * (size_t)(nset + 1));
+    int *ey = (int *)malloc(sizeof(int) * (size_t)(nset + 1));
+    int64_t m = 0;
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++)
+            if (E_df[(size_t)y * W + x]) { ex[m] = x; ey[m] = y; m++; }
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            int64_t best = ORACLE_NO_EDGE;
+            for (int64_t i = 0; i < m; i++) {
+                int64_t dx = x - ex[i], dy = y - ey[i];
+                int64_t d = dx * dx + dy * dy;
+                if (best < 0 || d < best) best = d;
+            }
+            D2[(size_t)y * W + x] = best;
+        }
+    free(ex); free(ey);
+}
+
+/* ---- Eq. (1): d_exp = 1 - exp(-d_Euc / alpha) ------------------------------
+ * d_Euc = sqrt(D2) in pixels; a frame with no edge pixel is fully saturated (S = 1,
+ * reading R5: the limit d_Euc -> inf). */
+void oracle_surface(const int64_t *D2, int64_t n, double alpha, double *S)
+{
+    for (int64_t i = 0; i < n; i++) {
+        if (D2[i] == ORACLE_NO_EDGE) {
+            S[i] = 1.0;
+        } else {
+            double d_euc = sqrt((double)D2[i]);
+            S[i] = 1.0 - exp(-d_euc / alpha);
+        }
+    }
+}
+
+/* ---- Eq. (2)-(3): alpha = -d_sat / ln(eps), eps = 1/255 --------------------
+ * The paper prints alpha ~ d_sat / 5.541, i.e. ln 255 = 5.5413; the oracle keeps
+ * the full-precision ln (reading R6).  d_sat <= 0 (or NaN) returns NaN. */
+double oracle_alpha_from_dsat(double d_sat)
+{
+    const double eps = 1.0 / 255.0;
+    if (!(d_sat > 0.0)) return NAN;
+    return -d_sat / log(eps);
+}
+
+/* Composition of the whole path for one window, in the paper's order (Fig. 1):
+ * accumulate -> denoise (Alg. 1) -> fill (Alg. 2) -> EDT -> Eq. (1).
+ * Any of E, E_d, E_df, D2 may be NULL (scratch is allocated); S may be NULL. */
+int oracle_build_window(const uint32_t *xy, int64_t n, int W, int H, int N_d, int N_f,
+                        double alpha, uint8_t *E, uint8_t *E_d, uint8_t *E_df, int64_t *D2,
+                        double *S)
+{
+    if (W <= 0 || H <= 0 || N_d < 0 || N_d > 4 || N_f < 1 || N_f > 5 || !(alpha > 0.0))
+        return ORACLE_EINVAL;
+    size_t npx = (size_t)W * (size_t)H;
+    uint8_t *e = E ? E : (uint8_t *)malloc(npx);
+    uint8_t *ed = E_d ? E_d : (uint8_t *)malloc(npx);
+    uint8_t *edf = E_df ? E_df : (uint8_t *)malloc(npx);
+    int64_t *d2 = D2 ? D2 : (int64_t *)malloc(sizeof(int64_t) * npx);
+    int st = oracle_accumulate(xy, n, W, H, e);
+    oracle_denoise(e, W, H, N_d, ed);
+    oracle_fill(ed, W, H, N_f, edf);
+    oracle_edt_separable(edf, W, H, d2);
+    if (S) oracle_surface(d2, (int64_t)npx, alpha, S);
+    if (!E) free(e);
+    if (!E_d) free(ed);
+    if (!E_df) free(edf);
+    if (!D2) free(d2);
+    return st;
+}

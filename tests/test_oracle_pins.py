@@ -1,0 +1,284 @@
+"""Pins for the CPU oracle (oracle/): each oracle function is checked against something
+other than itself -- hand-worked fixtures from the paper's algorithms (tests/golden/),
+brute force, library routines (numpy / scipy), closed forms and invariants.
+
+Citations: P:N = /root/reference/PAPER.md line N; S:N = SPEC.md line N (test ideas only).
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import ndimage
+
+import oracle
+from synth.events import pack_xy, random_frame_events, window_events, WORKLOADS
+from tests import golden
+
+K4 = np.array([[0, 1, 0], [1, 0, 1], [0, 1, 0]])
+
+
+def rand_frame(rng, h, w, p):
+    return (rng.random((h, w)) < p).astype(np.uint8)
+
+
+# ---------------------------------------------------------------- accumulation
+
+def test_accumulate_distinct_pixels():
+    # "binary matrices indicate whether or not each pixel produced at least one event"
+    xy = random_frame_events(97, 61, 0.1, seed=3, dup=2.0)
+    E = oracle.accumulate(xy, 97, 61)
+    assert E.sum() == len(np.unique(xy))
+    x, y = xy & 0xFFFF, xy >> 16
+    ref = np.zeros((61, 97), np.uint8)
+    ref[y, x] = 1
+    assert np.array_equal(E, ref)
+
+
+def test_accumulate_duplication_and_order_invariant():
+    rng = np.random.default_rng(0)
+    xy = random_frame_events(50, 40, 0.2, seed=4, dup=0.0)
+    E1 = oracle.accumulate(xy, 50, 40)
+    xy2 = np.concatenate([xy, xy[rng.integers(0, len(xy), 500)]])
+    rng.shuffle(xy2)
+    assert np.array_equal(E1, oracle.accumulate(xy2, 50, 40))
+
+
+def test_accumulate_polarity_ignored_same_pixel_set_once():
+    # two events at one pixel with opposite polarity -> that pixel set once;
+    # the oracle never sees polarity, so the pixel is set exactly once.
+    xy = pack_xy([5, 5], [7, 7])
+    E = oracle.accumulate(xy, 10, 10)
+    assert E.sum() == 1 and E[7, 5] == 1
+
+
+def test_accumulate_out_of_frame_rejected():
+    with pytest.raises(oracle.OracleRangeError):
+        oracle.accumulate(pack_xy([10], [0]), 10, 10)
+    with pytest.raises(oracle.OracleRangeError):
+        oracle.accumulate(pack_xy([0], [10]), 10, 10)
+
+
+# ---------------------------------------------------------------- Alg. 1 / Alg. 2
+
+@pytest.mark.parametrize("name", ["denoise_block3x3.txt", "fill_plus.txt", "order_counterexample.txt"])
+def test_golden_filters(name):
+    inp, blocks = golden.load(name)
+    for op, prm, lines in blocks:
+        exp = golden.image(lines)
+        if op == "denoise":
+            got = oracle.denoise(inp, prm["N_d"])
+        elif op == "fill":
+            got = oracle.fill(inp, prm["N_f"])
+        elif op == "denoise_fill":
+            got = oracle.fill(oracle.denoise(inp, prm["N_d"]), prm["N_f"])
+        else:
+            raise AssertionError(op)
+        assert got.sum() == prm["count"], (name, op, prm)
+        assert np.array_equal(got, exp), (name, op, prm)
+
+
+def test_order_counterexample_fused_differs():
+    # The fused single pass (fill counted on E instead of E_d) would give 7 pixels.
+    inp, _ = golden.load("order_counterexample.txt")
+    fused = oracle.denoise(inp, 1) | ((ndimage.convolve(inp.astype(int), K4, mode="constant") >= 4)
+                                      & (inp == 0)).astype(np.uint8)
+    assert fused.sum() == 7
+    assert oracle.fill(oracle.denoise(inp, 1), 4).sum() == 6
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 37), (29, 1), (17, 33), (64, 64), (60, 346)])
+def test_filters_match_library_convolution(shape):
+    # n_d / n_f = 4-neighbour count with zero outside the frame = convolution with the
+    # cross kernel, mode='constant' (library routine), thresholds as in P:128.
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    for p in (0.05, 0.3, 0.7):
+        E = rand_frame(rng, *shape, p)
+        cnt = ndimage.convolve(E.astype(int), K4, mode="constant", cval=0)
+        for nd in range(5):
+            Ed = oracle.denoise(E, nd)
+            assert np.array_equal(Ed, (E & (cnt >= nd)).astype(np.uint8))
+            cnt2 = ndimage.convolve(Ed.astype(int), K4, mode="constant", cval=0)
+            for nf in range(1, 6):
+                Edf = oracle.fill(Ed, nf)
+                assert np.array_equal(Edf, (Ed | (cnt2 >= nf)).astype(np.uint8))
+
+
+def test_filter_special_cases_and_invariants():
+    rng = np.random.default_rng(7)
+    E = rand_frame(rng, 40, 53, 0.25)
+    # N_d = 0 disables denoising, N_f = 5 disables filling
+    assert np.array_equal(oracle.denoise(E, 0), E)
+    assert np.array_equal(oracle.fill(E, 5), E)
+    # isolated pixel removed for any N_d >= 1
+    lone = np.zeros((9, 9), np.uint8)
+    lone[4, 4] = 1
+    for nd in range(1, 5):
+        assert oracle.denoise(lone, nd).sum() == 0
+    # empty stays empty under filling
+    assert oracle.fill(np.zeros((8, 8), np.uint8), 1).sum() == 0
+    prev = None
+    for nd in range(5):
+        Ed = oracle.denoise(E, nd)
+        assert np.all(Ed <= E)                        # E_d subset of E
+        if prev is not None:
+            assert np.all(Ed <= prev)                 # monotone in N_d
+        prev = Ed
+        # rotation / transpose invariance of the 4-neighbourhood
+        assert np.array_equal(oracle.denoise(np.rot90(E).copy(), nd), np.rot90(Ed))
+        assert np.array_equal(oracle.denoise(E.T.copy(), nd), Ed.T)
+    prev = None
+    for nf in range(1, 6):
+        Edf = oracle.fill(E, nf)
+        assert np.all(Edf >= E)                       # E_df superset of E_d
+        if prev is not None:
+            assert np.all(Edf <= prev)                # raising N_f never adds pixels
+        prev = Edf
+        assert np.array_equal(oracle.fill(np.rot90(E).copy(), nf), np.rot90(Edf))
+
+
+# ---------------------------------------------------------------- EDT (§III-C)
+
+def brute_d2_numpy(E):
+    """Independent brute force: min over edge pixels of squared Euclidean distance."""
+    ys, xs = np.nonzero(E)
+    h, w = E.shape
+    if len(xs) == 0:
+        return np.full((h, w), oracle.NO_EDGE, np.int64)
+    gy, gx = np.mgrid[0:h, 0:w]
+    d = (gx.reshape(-1, 1) - xs.reshape(1, -1)) ** 2 + (gy.reshape(-1, 1) - ys.reshape(1, -1)) ** 2
+    return d.min(axis=1).reshape(h, w).astype(np.int64)
+
+
+def scipy_d2(E):
+    """Exact integer D2 from scipy's exact EDT nearest-feature indices (library routine)."""
+    if E.sum() == 0:
+        return np.full(E.shape, oracle.NO_EDGE, np.int64)
+    _, (iy, ix) = ndimage.distance_transform_edt(E == 0, return_indices=True)
+    gy, gx = np.mgrid[0:E.shape[0], 0:E.shape[1]]
+    return ((iy - gy).astype(np.int64) ** 2 + (ix - gx).astype(np.int64) ** 2)
+
+
+def test_golden_edt_345():
+    inp, blocks = golden.load("edt_345.txt")
+    exp = golden.ints(blocks[0][2])
+    got = oracle.edt(inp)
+    assert np.array_equal(got, exp)
+    assert got[4, 3] == 25
+
+
+def test_edt_bruteforce_200_random_frames():
+    # 200 seeded 64x64 frames, 1-50 % density, zero tolerance
+    rng = np.random.default_rng(2024)
+    for i in range(200):
+        p = [0.01, 0.03, 0.1, 0.25, 0.5][i % 5]
+        h, w = (64, 64) if i % 4 else (int(rng.integers(1, 65)), int(rng.integers(1, 65)))
+        E = rand_frame(rng, h, w, p)
+        exp = brute_d2_numpy(E)
+        assert np.array_equal(oracle.edt(E), exp), i
+        assert np.array_equal(oracle.edt_bruteforce(E), exp), i
+
+
+def test_edt_matches_scipy_on_workload_frames():
+    # full-size frames shaped like the paper's workloads, vs scipy's exact EDT
+    for name in ("C1", "C3"):
+        wl = WORKLOADS[name]
+        c = wl.scene
+        xy = window_events(c, wl.seed, 0)
+        Edf = oracle.fill(oracle.denoise(oracle.accumulate(xy, c.width, c.height), wl.n_d), wl.n_f)
+        assert np.array_equal(oracle.edt(Edf), scipy_d2(Edf))
+
+
+def test_edt_special_cases_and_invariants():
+    assert np.all(oracle.edt(np.ones((7, 9), np.uint8)) == 0)             # all set -> 0
+    assert np.all(oracle.edt(np.zeros((7, 9), np.uint8)) == oracle.NO_EDGE)  # empty -> sentinel
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        E = rand_frame(rng, 37, 45, 0.02)
+        E[rng.integers(0, 37), rng.integers(0, 45)] = 1
+        D = oracle.edt(E)
+        assert np.all((D == 0) == (E == 1))                                 # 0 exactly on edges
+        # adding edge pixels never increases a distance
+        E2 = E | rand_frame(rng, 37, 45, 0.01)
+        assert np.all(oracle.edt(E2) <= D)
+        # 1-Lipschitz: 4-adjacent pixels differ by at most 1 in distance
+        d = np.sqrt(D.astype(float))
+        assert np.all(np.abs(np.diff(d, axis=0)) <= 1 + 1e-12)
+        assert np.all(np.abs(np.diff(d, axis=1)) <= 1 + 1e-12)
+
+
+# ---------------------------------------------------------------- Eq. (1)-(3)
+
+def test_alpha_from_dsat_paper_constants():
+    # Eq. (3): alpha ~ d_sat / 5.541; alpha = 1.08 for d_sat = 6 px
+    a6 = oracle.alpha_from_dsat(6.0)
+    assert abs(a6 - 1.08) < 5e-3
+    assert abs(6.0 / a6 - 5.541) < 5e-4
+    # Eq. (2) with eps = 1/255: d_sat = ln 255 gives alpha = 1 exactly
+    assert abs(oracle.alpha_from_dsat(math.log(255.0)) - 1.0) < 1e-15
+    assert abs(oracle.alpha_from_dsat(12.0) - 2 * a6) < 1e-15               # linear in d_sat
+    assert math.isnan(oracle.alpha_from_dsat(0.0)) and math.isnan(oracle.alpha_from_dsat(-1.0))
+
+
+def test_surface_saturation_gap_is_eps():
+    # At d_Euc = d_sat the gap to saturation is eps = 1/255 (definition of eps):
+    # d_exp = 1 - eps.  On 8 bits: q(d_sat) = 254, q(d_sat + 1) = 255.
+    for d_sat in (3, 6, 9, 12):
+        a = oracle.alpha_from_dsat(float(d_sat))
+        S = oracle.surface(np.array([d_sat * d_sat, (d_sat + 1) ** 2]), a)
+        assert abs(S[0] - 254.0 / 255.0) < 1e-14
+        assert int(math.floor(255 * S[0] + 0.5)) == 254
+        if d_sat == 6:
+            assert int(math.floor(255 * S[1] + 0.5)) == 255
+
+
+def test_surface_values_and_shape():
+    # d = 0 -> 0 exactly on edge pixels; alpha = 2, d = 2 -> 1 - 1/e (Fig. 4)
+    S = oracle.surface(np.array([0, 4, oracle.NO_EDGE]), 2.0)
+    assert S[0] == 0.0
+    assert abs(S[1] - (1.0 - 1.0 / math.e)) < 1e-15
+    assert S[2] == 1.0                                                       # empty frame: saturated
+    # monotone non-decreasing in D2, values in [0, 1) ("saturate to a value of 1")
+    d2 = np.arange(0, 5000, dtype=np.int64)
+    S = oracle.surface(d2, oracle.alpha_from_dsat(6.0))
+    assert np.all(np.diff(S) >= 0) and S[0] == 0 and np.all(S <= 1.0)
+    # strictly below 1 wherever fp64 can represent the gap exp(-d/alpha) > 2^-53
+    assert np.all(S[d2 < (30 * oracle.alpha_from_dsat(6.0)) ** 2] < 1.0)
+    # north-star invariant on eps = 1 - S (conflict C1): maximal (1) on edge pixels, decreasing
+    eps = 1.0 - S
+    assert eps[0] == 1.0 and np.all(np.diff(eps) <= 0)
+
+
+def test_isolated_event_closed_form():
+    # One event, N_d = 0 (no denoising) and N_f = 2 (a lone pixel's neighbours have n_f = 1):
+    # the edge image is that pixel, so S(x,y) = 1 - exp(-|(x,y)-(x0,y0)| / alpha)  (Eq. (1)).
+    W, H, x0, y0 = 41, 23, 17, 5
+    a = oracle.alpha_from_dsat(6.0)
+    out = oracle.build_window(pack_xy([x0], [y0]), W, H, 0, 2, a)
+    assert out["E_df"].sum() == 1
+    for y in range(H):
+        for x in range(W):
+            exp = 1.0 - math.exp(-math.hypot(x - x0, y - y0) / a)
+            assert abs(out["S"][y, x] - exp) < 1e-15
+    # with the paper's N_d = 1 the lone event is noise and is removed: S == 1 everywhere
+    out = oracle.build_window(pack_xy([x0], [y0]), W, H, 1, 4, a)
+    assert out["E_df"].sum() == 0 and np.all(out["S"] == 1.0)
+
+
+def test_build_window_composes_steps():
+    wl = WORKLOADS["C1"]
+    c = wl.scene
+    xy = window_events(c, wl.seed, 0)
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    out = oracle.build_window(xy, c.width, c.height, wl.n_d, wl.n_f, a)
+    E = oracle.accumulate(xy, c.width, c.height)
+    Ed = oracle.denoise(E, wl.n_d)
+    Edf = oracle.fill(Ed, wl.n_f)
+    D2 = oracle.edt(Edf)
+    assert np.array_equal(out["E"], E) and np.array_equal(out["E_d"], Ed)
+    assert np.array_equal(out["E_df"], Edf) and np.array_equal(out["D2"], D2)
+    assert np.array_equal(out["S"], oracle.surface(D2, a))
+    # the batch helper (thread pool) reproduces per-window results
+    xy2 = np.concatenate([xy, window_events(c, wl.seed, 1)])
+    offs = np.array([0, len(xy), len(xy2)])
+    res = oracle.build_batch(xy2, offs, c.width, c.height, wl.n_d, wl.n_f, a, threads=2)
+    assert np.array_equal(res[0]["S"], out["S"])
