@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the batched IEDS build (BASELINE.json metric: IEDS surfaces/s and Mev/s at
+1280x720, % of HBM peak).
+
+One "step" = the whole hot path (scatter -> denoise -> fill -> exact EDT -> Eq. (1)) over one
+batch of synthetic windows already resident in HBM: workload C3 (1280x720 Gen4-like, 1000
+windows x 75k events per GPU; N_d=2, N_f=3, d_sat=6).  Multi-GPU: one
+process per GPU (torchrun), each rank processes its own 1000 distinct windows (weak scaling,
+windows are independent: no collective in the data path); timing = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+--impl reference times the CPU oracle (the reference arm of this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.events import WORKLOADS, batch_events  # noqa: E402
+
+METRIC = "IEDS surfaces/sec and Mev/s at 1280x720 (1/2/4/8 B200), % HBM peak"
+UNIT = "surfaces/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------- inputs
+
+def _gen_part(args):
+    name, k0, n = args
+    wl = WORKLOADS[name]
+    return batch_events(wl.scene, wl.seed, k0, n)
+
+
+def generate(name: str, k0: int, n: int, procs: int | None = None):
+    """Windows k0..k0+n-1 of workload `name` as CSR, generated on a process pool."""
+    import multiprocessing as mp
+
+    procs = procs or max(1, min(len(os.sched_getaffinity(0)), 32))
+    per = max(1, math.ceil(n / (procs * 4)))
+    parts = [(name, k0 + i, min(per, n - i)) for i in range(0, n, per)]
+    if procs == 1 or len(parts) == 1:
+        res = [_gen_part(p) for p in parts]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_gen_part, parts)
+    xy = np.concatenate([r[0] for r in res])
+    off = np.zeros(n + 1, np.int64)
+    pos, i = 0, 0
+    for r in res:
+        m = len(r[1]) - 1
+        off[i + 1:i + m + 1] = r[1][1:] + pos
+        pos += len(r[0])
+        i += m
+    return xy, off
+
+
+# ------------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, pw = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------------------- oracle baseline
+
+def _oracle_windows(args):
+    name, k0, n = args
+    import oracle
+
+    wl = WORKLOADS[name]
+    c = wl.scene
+    xy, off = batch_events(c, wl.seed, k0, n)
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    t = time.perf_counter()
+    for b in range(n):
+        oracle.build_window(xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a, want=("S",))
+    return time.perf_counter() - t
+
+
+def oracle_rate(name: str, n_windows: int, cores: int, pool=None):
+    """Time the oracle (as it stands) on `n_windows` windows spread over `cores` processes.
+    Event generation happens inside the workers before their clock starts."""
+    import multiprocessing as mp
+
+    per = max(1, n_windows // cores)
+    jobs = [(name, 7919 * i, per) for i in range(cores)]
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
+    t0 = time.perf_counter()
+    per_times = pool.map(_oracle_windows, jobs)
+    wall = time.perf_counter() - t0
+    if own:
+        pool.close()
+        pool.join()
+    done = per * cores
+    # the workers' compute time excludes their generation time
+    busy = max(per_times)
+    return done / busy, done, wall
+
+
+# ------------------------------------------------------------------------------- arms
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+
+    wl = WORKLOADS[args.config]
+    cores = len(os.sched_getaffinity(0))
+    pool = mp.get_context("fork").Pool(cores)
+    for _ in range(args.warmup):
+        oracle_rate(args.config, cores, cores, pool)
+    rates, walls = [], []
+    for _ in range(args.steps):
+        r, done, wall = oracle_rate(args.config, cores, cores, pool)
+        rates.append(r)
+        walls.append(wall)
+    pool.close()
+    pool.join()
+    value = statistics.median(rates)
+    c = wl.scene
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {c.width}x{c.height}, {c.events_per_window} events/window",
+                   "width": c.width, "height": c.height, "n_d": wl.n_d, "n_f": wl.n_f, "d_sat": wl.d_sat},
+        "mev_per_s": value * c.events_per_window / 1e6,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step: {cores} windows of {wl.name}, one process per core, "
+                                   "C oracle (fp64) as it stands"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2112_10591_b200 as ieds
+
+    wl = WORKLOADS[args.config]
+    c = wl.scene
+    W, H = c.width, c.height
+    nwin = args.windows or wl.n_windows
+    k0 = rank * nwin
+    xy, off = generate(args.config, k0, nwin)
+    n_ev = len(xy)
+    txy = torch.from_numpy(xy.view(np.int32)).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    S = torch.empty((nwin, H, W), dtype=torch.float32, device=dev)
+    bld = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        bld.build_batch(txy, toff, S)
+    bld.sync()
+    torch.cuda.synchronize(dev)
+
+    launches_per_step = bld.launches_per_batch(nwin)
+    bld.profile(True)
+    bld.profile_read()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        bld.build_batch(txy, toff, S)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    prof = bld.profile_read()
+    bld.profile(False)
+    bld.sync()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    total_windows = nwin * world
+    value = total_windows / (ms_step / 1e3)
+
+    # roofline of the dominant kernel (EDT + surface, a4-a5): algorithmic bytes = 4 B/px fp32 surface
+    peak, peak_src = peaks()
+    edt_ms, edt_n = prof["edt"]
+    fr_ms, fr_n = prof["frame"]
+    chunk_windows = math.ceil(nwin / max(1, edt_n // max(1, args.steps)))
+    edt_avg_ms = edt_ms / max(1, edt_n)
+    edt_bytes_per_launch = 4.0 * W * H * (nwin / max(1, edt_n // args.steps))
+    edt_gbs = edt_bytes_per_launch / (edt_avg_ms / 1e3) / 1e9
+    fr_avg_ms = fr_ms / max(1, fr_n)
+    fr_bytes_per_launch = 4.0 * n_ev / max(1, fr_n // args.steps)
+    path_bytes = 4.0 * n_ev + 4.0 * W * H * nwin + 8.0 * (nwin + 1)
+    path_gbs = path_bytes / (ms_step / 1e3) / 1e9
+
+    # end to end through the C ABI with host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hxy = torch.from_numpy(xy.view(np.int32)).pin_memory()
+        hoff = torch.from_numpy(off).pin_memory()
+        hS = torch.empty((nwin, H, W), dtype=torch.float32).pin_memory()
+        nxy, noff, nS = hxy.numpy().view(np.uint32), hoff.numpy(), hS.numpy()
+        bld.build_batch_host(nxy, noff, nS)
+        esteps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(esteps):
+            bld.build_batch_host(nxy, noff, nS)
+        el = (time.perf_counter() - t0) / esteps
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te.item())
+        e2e = {"value": total_windows / el, "unit": UNIT, "h2d_bytes_per_step": int(4 * n_ev + 8 * (nwin + 1)),
+               "d2h_bytes_per_step": int(4 * W * H * nwin), "steps": esteps,
+               "note": "ieds_build_batch_host: pinned host events in, pinned host surfaces out, per rank"}
+        del hxy, hoff, hS
+
+    bld.close()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        n_s = cores * max(1, args.cpu_windows_per_core)
+        r, done, wall = oracle_rate(args.config, n_s, cores)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{done} windows of {wl.name} (distinct seeds), {cores} processes, "
+                         f"C oracle fp64 as it stands, {wall:.1f} s wall"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32+i32+f32", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {W}x{H} Gen4-like, {nwin} windows x {c.events_per_window} events per GPU",
+                   "windows_per_gpu": nwin, "events_per_gpu": n_ev, "width": W, "height": H, "n_d": wl.n_d,
+                   "n_f": wl.n_f, "d_sat": wl.d_sat, "alpha": bld.params.alpha,
+                   "l2": "inputs+outputs larger than L2 (events %.0f MB, surfaces %.0f MB per step)" % (
+                       4 * n_ev / 1e6, 4 * W * H * nwin / 1e6)},
+        "mev_per_s": value * (n_ev / nwin) / 1e6,
+        "hbm_frac_path": {"achieved_gbs": path_gbs, "peak": peak, "frac": path_gbs / peak,
+                          "frac_nominal_8tbs": path_gbs / 8000.0,
+                          "bytes_per_window": path_bytes / nwin,
+                          "note": "algorithmic bytes of the whole path: 4 B/event + 4 B/px + offsets"},
+        "roofline": {"bound": "hbm", "kernel": "edt_kernel (a4 exact EDT + a5 surface)",
+                     "achieved": edt_gbs, "peak": peak, "unit": "GB/s", "frac": edt_gbs / peak,
+                     "traffic": args.traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": edt_bytes_per_launch, "avg_launch_ms": edt_avg_ms,
+                     "share_of_step": edt_ms / max(1e-9, ms_max)},
+        "kernels": {"frame_kernel": {"avg_ms": fr_avg_ms, "launches": fr_n,
+                                     "achieved_gbs": fr_bytes_per_launch / (fr_avg_ms / 1e3) / 1e9 if fr_avg_ms else None,
+                                     "share_of_step": fr_ms / max(1e-9, ms_max)},
+                    "edt_kernel": {"avg_ms": edt_avg_ms, "launches": edt_n}},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--windows", type=int, default=0, help="override windows per GPU (default: config)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-windows-per-core", type=int, default=4)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per EDT launch (from profiles/), reported in roofline.traffic")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing protocol", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

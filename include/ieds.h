@@ -1,0 +1,130 @@
+/*
+ * ieds.h -- C ABI of the batched inverse-exponential-distance-surface (IEDS) build.
+ *
+ * Operation (Brebion et al., arXiv 2112.10591; "P:N" = /root/reference/PAPER.md line N):
+ * for every time window of events, independently,
+ *   a1  edge image E: pixel = 1 iff at least one event of the window fell on it, polarity
+ *       ignored (§III-A);
+ *   a2  denoising (Algorithm 1): E_d[p] = E[p] and n4_E(p) >= N_d;
+ *   a3  filling   (Algorithm 2): E_df[p] = E_d[p] or n4_{E_d}(p) >= N_f,
+ *       strictly after a2; out-of-frame neighbours count as non-edge;
+ *   a4  exact Euclidean distance transform to the closest E_df pixel (§III-C),
+ *       as an exact integer squared distance D2;
+ *   a5  surface S = 1 - exp(-sqrt(D2) / alpha) (Eq. (1)), fp32.
+ * A window whose E_df is empty has D2 = IEDS_NO_EDGE everywhere and S = 1 (saturated).
+ * alpha may be derived from the saturation distance with ieds_alpha_from_dsat (Eq. (2)-(3),
+ * P:228-233).
+ *
+ * Memory model: every array argument of ieds_build_batch is a DEVICE pointer owned by the
+ * caller (e.g. a torch tensor); ieds_build_batch_host takes HOST pointers.  The handle owns
+ * only its scratch.  Layouts:
+ *   events_xy       uint32 [n_events], packed x | (y << 16), x = column, y = row; the
+ *                   events of window b are events_xy[window_offsets[b] .. window_offsets[b+1]).
+ *   window_offsets  int64 [num_windows + 1], offsets[0] >= 0, non-decreasing,
+ *                   offsets[num_windows] <= n_events; empty windows are allowed.
+ *   surfaces        float32 [num_windows][height][width], row-major.
+ *   *_bits          uint32 [num_windows][height][ceil(width/32)]: bit (x % 32) of word x/32
+ *                   is pixel x (LSB = lowest x); padding bits beyond width are 0.
+ *   sqdist          uint32 [num_windows][height][width]: exact D2, IEDS_NO_EDGE if the
+ *                   window's E_df is empty.
+ *
+ * Errors: functions return IEDS_OK (0) or a negative code.  Argument errors are detected on
+ * the host before anything is enqueued.  Data errors found on the device (an event outside
+ * the frame -> IEDS_ERANGE, event dropped; bad offsets -> IEDS_EORDER, window left empty)
+ * are latched in the handle and returned by the next ieds_sync.
+ *
+ * Threading: a handle may be used by one host thread at a time; calls on one handle must be
+ * issued on streams that are ordered with respect to each other (the scratch is shared).
+ * Handles on different devices are independent.
+ */
+#ifndef IEDS_H
+#define IEDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IEDS_NO_EDGE 0xFFFFFFFFu
+
+enum {
+    IEDS_OK = 0,
+    IEDS_EINVAL = -1,    /* invalid argument / configuration                          */
+    IEDS_ERANGE = -2,    /* an event lies outside the width x height frame (device)    */
+    IEDS_ECAPACITY = -3, /* batch exceeds a host-API capacity                          */
+    IEDS_EORDER = -4,    /* window_offsets not non-decreasing / out of [0, n_events]   */
+    IEDS_ECUDA = -5,     /* a CUDA runtime call failed                                  */
+    IEDS_ENOMEM = -6     /* device or pinned allocation failed                          */
+};
+
+typedef struct ieds_handle ieds_handle; /* opaque */
+
+typedef struct {
+    int32_t width;          /* 1 .. 4096 pixels                                         */
+    int32_t height;         /* 1 .. 2048 pixels; ceil(width/32)*height words must fit in */
+                            /* one CTA's shared memory (ieds_create checks)             */
+    int32_t n_d;            /* 0 .. 4, denoising threshold N_d (0 disables)       */
+    int32_t n_f;            /* 1 .. 5, filling threshold N_f (5 disables)         */
+    double alpha;           /* > 0 and finite, spreading parameter of Eq. (1), pixels    */
+    int32_t chunk_windows;  /* windows processed per launch pair (sizes the scratch);    */
+                            /* batches of any size are processed chunk by chunk. 0 = 128 */
+    int32_t device;         /* CUDA device ordinal; -1 = current device                 */
+} ieds_config;
+
+/* Validates cfg, allocates the scratch on cfg->device and builds the Eq. (1) table.
+ * On success *out is a new handle; on failure *out is NULL. */
+int ieds_create(const ieds_config *cfg, ieds_handle **out);
+
+/* NULL-safe.  Synchronises the device before freeing. */
+void ieds_destroy(ieds_handle *h);
+
+/* Enqueue the whole path a1..a5 for num_windows windows on `stream` (a cudaStream_t;
+ * NULL = legacy default stream).  DEVICE pointers.  surfaces is required; edge_bits,
+ * denoised_bits, filtered_bits and sqdist are optional (NULL = not produced).  No host
+ * synchronisation and no allocation: the call is CUDA-graph capturable.  num_windows = 0
+ * is a no-op. */
+int ieds_build_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *window_offsets,
+                     int64_t n_events, int32_t num_windows, float *surfaces, uint32_t *edge_bits,
+                     uint32_t *denoised_bits, uint32_t *filtered_bits, uint32_t *sqdist,
+                     void *stream);
+
+/* Same operation with HOST pointers (events_xy, window_offsets, surfaces): the library
+ * copies events in and surfaces out chunk by chunk, overlapping the copies with the
+ * kernels on internal streams, and returns when the surfaces are in host memory.
+ * Page-locked host buffers give full PCIe bandwidth.  Grows internal buffers as needed
+ * (this entry point may allocate).  Returns data errors directly (no ieds_sync needed). */
+int ieds_build_batch_host(ieds_handle *h, const uint32_t *events_xy,
+                          const int64_t *window_offsets, int32_t num_windows, float *surfaces);
+
+/* Wait for `stream`, then return (and clear) the latched device error, or IEDS_OK. */
+int ieds_sync(ieds_handle *h, void *stream);
+
+/* Number of kernel launches ieds_build_batch issues for num_windows windows. */
+int64_t ieds_launches_per_batch(const ieds_handle *h, int32_t num_windows);
+
+/* Per-kernel device timing (tracing).  While enabled, ieds_build_batch records a CUDA event
+ * pair around every kernel it launches (on the caller's stream; the event pool grows as
+ * needed, so this mode may allocate).  ieds_profile_read waits for the recorded events and
+ * returns the summed device time in ms and the launch count of each kernel since the last
+ * read, then resets the counters.  kernel 0 = frame (a1-a3), kernel 1 = EDT + surface (a4-a5).
+ * Any output pointer may be NULL. */
+int ieds_profile_enable(ieds_handle *h, int on);
+int ieds_profile_read(ieds_handle *h, double *frame_ms, int64_t *frame_launches, double *edt_ms,
+                      int64_t *edt_launches);
+
+/* Static description of an error code. */
+const char *ieds_strerror(int code);
+
+/* Eq. (2)-(3): alpha = -d_sat / ln(1/255) = d_sat / ln 255.  NaN if d_sat <= 0
+ * or not finite. */
+double ieds_alpha_from_dsat(double d_sat);
+
+/* Library / kernel build identification string. */
+const char *ieds_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IEDS_H */

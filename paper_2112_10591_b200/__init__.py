@@ -1,0 +1,171 @@
+"""B200-native batched IEDS build (Brebion et al., arXiv 2112.10591).
+
+Thin binding over the C ABI of include/ieds.h: it only marshals torch tensors (device
+memory, streams) into the library's calls.  Every step of the path -- scatter, denoise
+(Alg. 1), fill (Alg. 2), exact EDT and the Eq. (1) surface -- runs in the CUDA kernels of
+libieds.so.  There is no CPU fallback: without the library or a CUDA device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+from ._lib import (IEDS_NO_EDGE, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
+                   check, load)
+
+__all__ = ["Builder", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
+           "IEDS_NO_EDGE", "LIB_PATH"]
+
+load()   # fail loudly at import if libieds.so is missing
+
+
+def alpha_from_dsat(d_sat: float) -> float:
+    """Eq. (2)-(3): alpha = d_sat / ln 255."""
+    return load().ieds_alpha_from_dsat(float(d_sat))
+
+
+def version() -> str:
+    return load().ieds_version().decode()
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@dataclasses.dataclass
+class Params:
+    width: int
+    height: int
+    n_d: int
+    n_f: int
+    alpha: float
+
+
+class Builder:
+    """One ieds_handle on one CUDA device.
+
+    Builder(width, height, n_d, n_f, alpha=None, d_sat=6.0) -- alpha defaults to
+    alpha_from_dsat(d_sat).  build_batch() enqueues on the current torch stream (or the
+    given one) and does not synchronise; sync() reports latched device errors.
+    """
+
+    def __init__(self, width: int, height: int, n_d: int, n_f: int, alpha: float | None = None,
+                 d_sat: float = 6.0, chunk_windows: int = 0, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2112_10591_b200 needs a CUDA device (no CPU fallback)")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", torch.device(device).index if not isinstance(device, int) else device)
+        if alpha is None:
+            alpha = alpha_from_dsat(d_sat)
+        self.params = Params(width, height, n_d, n_f, float(alpha))
+        cfg = IedsConfig(width, height, n_d, n_f, float(alpha), chunk_windows, self.device.index)
+        h = ctypes.c_void_p()
+        check(load().ieds_create(ctypes.byref(cfg), ctypes.byref(h)), "ieds_create")
+        self._h = h
+        self.width, self.height = width, height
+        self.words = (width + 31) // 32
+
+    # -- lifecycle -------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            load().ieds_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- helpers ---------------------------------------------------------------------------
+    def _stream(self, stream):
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(stream.cuda_stream)
+
+    def _check_dev(self, t, name, dtypes):
+        if t is None:
+            return
+        if not t.is_cuda or t.device != self.device:
+            raise ValueError(f"{name} must be a tensor on {self.device}")
+        if t.dtype not in dtypes:
+            raise TypeError(f"{name} must have dtype in {dtypes}, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+
+    def profile(self, on: bool = True):
+        """Enable/disable per-kernel CUDA-event timing inside the library."""
+        check(load().ieds_profile_enable(self._h, 1 if on else 0), "ieds_profile_enable")
+
+    def profile_read(self) -> dict:
+        """{'frame': (ms, launches), 'edt': (ms, launches)} since the last read."""
+        fm, em = ctypes.c_double(), ctypes.c_double()
+        fn, en = ctypes.c_int64(), ctypes.c_int64()
+        check(load().ieds_profile_read(self._h, ctypes.byref(fm), ctypes.byref(fn), ctypes.byref(em),
+                                       ctypes.byref(en)), "ieds_profile_read")
+        return {"frame": (fm.value, fn.value), "edt": (em.value, en.value)}
+
+    def launches_per_batch(self, num_windows: int) -> int:
+        return int(load().ieds_launches_per_batch(self._h, int(num_windows)))
+
+    # -- the path --------------------------------------------------------------------------
+    def build_batch(self, events_xy, offsets, out=None, *, edge_bits=None, denoised_bits=None,
+                    filtered_bits=None, sqdist=None, stream=None):
+        """Surfaces [B, H, W] fp32 for the CSR batch (events_xy uint32/int32 [n], offsets int64 [B+1]).
+
+        Optional outputs (pre-allocated, uint32/int32): edge_bits / denoised_bits /
+        filtered_bits [B, H, ceil(W/32)] (E, E_d, E_df) and sqdist [B, H, W] (exact D2,
+        0xFFFFFFFF when the window's E_df is empty).
+        """
+        import torch
+
+        u32 = (torch.int32, getattr(torch, "uint32", torch.int32))
+        self._check_dev(events_xy, "events_xy", u32)
+        self._check_dev(offsets, "offsets", (torch.int64,))
+        B = offsets.numel() - 1
+        if out is None:
+            out = torch.empty((B, self.height, self.width), dtype=torch.float32, device=self.device)
+        self._check_dev(out, "out", (torch.float32,))
+        if out.numel() < B * self.height * self.width:
+            raise ValueError("out too small")
+        for name, t, n in (("edge_bits", edge_bits, self.words), ("denoised_bits", denoised_bits, self.words),
+                           ("filtered_bits", filtered_bits, self.words), ("sqdist", sqdist, self.width)):
+            self._check_dev(t, name, u32)
+            if t is not None and t.numel() < B * self.height * n:
+                raise ValueError(f"{name} too small")
+        check(load().ieds_build_batch(self._h, _ptr(events_xy), _ptr(offsets), events_xy.numel(), B,
+                                      _ptr(out), _ptr(edge_bits), _ptr(denoised_bits), _ptr(filtered_bits),
+                                      _ptr(sqdist), self._stream(stream)), "ieds_build_batch")
+        return out
+
+    def sync(self, stream=None):
+        """Wait for the stream; raise IedsRangeError / IedsOrderError on latched data errors."""
+        check(load().ieds_sync(self._h, self._stream(stream)), "ieds_sync")
+
+    def build_batch_host(self, events_xy, offsets, out=None):
+        """Host-buffer entry point (ieds_build_batch_host): numpy uint32 [n], int64 [B+1] ->
+        float32 [B, H, W] host array; copies overlap the kernels inside the library."""
+        import numpy as np
+
+        xy = np.ascontiguousarray(events_xy).view(np.uint32)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        B = len(off) - 1
+        if out is None:
+            out = np.empty((B, self.height, self.width), np.float32)
+        if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < B * self.height * self.width:
+            raise ValueError("out must be a C-contiguous float32 array of B*H*W")
+        check(load().ieds_build_batch_host(self._h, xy.ctypes.data_as(ctypes.c_void_p),
+                                           off.ctypes.data_as(ctypes.c_void_p), B,
+                                           out.ctypes.data_as(ctypes.c_void_p)), "ieds_build_batch_host")
+        return out

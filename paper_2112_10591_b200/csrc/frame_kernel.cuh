@@ -1,0 +1,185 @@
+// frame_kernel.cuh -- rows a1..a3 of the hot path, one CTA per window.
+//
+//   a1 scatter   events -> bit-packed edge image E in shared memory      (§III-A)
+//   a2 denoise   E_d  = E   & [n4_E   >= N_d]                            (Alg. 1)
+//   a3 fill      E_df = E_d | [n4_E_d >= N_f]                            (Alg. 2)
+//   then         E_df is transposed into column words T (bit i of T[r][x] = E_df(x, 32r+i))
+//                plus a per-column bitmap of non-empty word-rows, which is all the EDT needs.
+//
+// Layout: the frame lives in shared memory as H rows of NWP = (ceil(W/32) | 1) words (an odd
+// row stride makes the "lane = row" accesses below bank-conflict free).  Bit (x % 32) of word
+// x / 32 is pixel x; bits beyond W stay 0.  Out-of-frame neighbours count as non-edge.
+#pragma once
+#include <cstdint>
+
+namespace ieds {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr int kErrRange = 1;   // an event outside the frame (dropped)
+constexpr int kErrOrder = 2;   // window offsets not non-decreasing / out of range
+
+struct FrameParams {
+    const uint32_t* __restrict__ xy;        // [n_events] x | y << 16
+    const int64_t* __restrict__ offsets;    // [nb + 1] absolute indices into xy
+    int64_t n_events;
+    int W, H, NW, NWP, NR, n_d, n_f;
+    int vec_ok;                             // xy is 16-byte aligned
+    uint32_t* __restrict__ T;               // [nb][NR][W] transposed E_df
+    unsigned long long* __restrict__ colmask;  // [nb][W] bit r = T[r][x] != 0
+    uint32_t* __restrict__ E_out;           // [nb][H][NW] or null
+    uint32_t* __restrict__ Ed_out;
+    uint32_t* __restrict__ Edf_out;
+    int* __restrict__ err;
+};
+
+// bit-sliced "at least n of the four neighbour words are set", per bit position
+__device__ __forceinline__ uint32_t at_least(int n, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    switch (n) {
+        case 0: return kFull;
+        case 1: return a | b | c | d;
+        case 2: return (a & b) | (c & d) | ((a | b) & (c | d));
+        case 3: return (a & b & (c | d)) | (c & d & (a | b));
+        case 4: return a & b & c & d;
+        default: return 0u;
+    }
+}
+
+__device__ __forceinline__ uint32_t frame_word(const uint32_t* fr, const FrameParams& p, int y, int w) {
+    return (y >= 0 && y < p.H && w >= 0 && w < p.NW) ? fr[y * p.NWP + w] : 0u;
+}
+
+// E_d word (y, w): Alg. 1 on 32 pixels at once.
+__device__ __forceinline__ uint32_t denoised_word(const uint32_t* fr, const FrameParams& p, int y, int w) {
+    uint32_t c = frame_word(fr, p, y, w);
+    uint32_t up = frame_word(fr, p, y - 1, w);
+    uint32_t dn = frame_word(fr, p, y + 1, w);
+    uint32_t lf = (c << 1) | (frame_word(fr, p, y, w - 1) >> 31);   // neighbour x-1
+    uint32_t rt = (c >> 1) | (frame_word(fr, p, y, w + 1) << 31);   // neighbour x+1
+    return c & at_least(p.n_d, up, dn, lf, rt);
+}
+
+// returns 1 if the event is outside the frame
+__device__ __forceinline__ uint32_t scatter_event(uint32_t* fr, const FrameParams& p, uint32_t v) {
+    uint32_t x = v & 0xFFFFu, y = v >> 16;
+    if (x < (uint32_t)p.W && y < (uint32_t)p.H) {
+        atomicOr(&fr[y * p.NWP + (x >> 5)], 1u << (x & 31));
+        return 0u;
+    }
+    return 1u;
+}
+
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* ptr) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
+    return r;
+}
+
+// 32x32 bit-matrix transpose across a warp: lane i holds row i on entry, column i on exit.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
+#define IEDS_TSTEP(s, m)                                                              \
+    {                                                                                 \
+        uint32_t o = __shfl_xor_sync(kFull, v, s);                                    \
+        v = (lane & s) ? ((v & ~(m)) | ((o & ~(m)) >> s)) : ((v & (m)) | ((o & (m)) << s)); \
+    }
+    IEDS_TSTEP(16, 0x0000FFFFu)
+    IEDS_TSTEP(8, 0x00FF00FFu)
+    IEDS_TSTEP(4, 0x0F0F0F0Fu)
+    IEDS_TSTEP(2, 0x33333333u)
+    IEDS_TSTEP(1, 0x55555555u)
+#undef IEDS_TSTEP
+    return v;
+}
+
+__global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int nframe = p.H * p.NWP;
+    uint32_t* fr = smem;
+    unsigned long long* cm = reinterpret_cast<unsigned long long*>(smem + ((nframe + 3) & ~3));
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+
+    // ---- clear the frame and the column bitmap
+    {
+        uint4 z = make_uint4(0, 0, 0, 0);
+        uint4* f4 = reinterpret_cast<uint4*>(fr);
+        const int n4 = (nframe + 3) >> 2;
+        for (int i = tid; i < n4; i += nthr) f4[i] = z;
+        for (int i = tid; i < p.W; i += nthr) cm[i] = 0ull;
+    }
+    __syncthreads();
+
+    // ---- a1: scatter this window's events (duplicates are idempotent; polarity absent)
+    int64_t o0 = p.offsets[b], o1 = p.offsets[b + 1];
+    if (o0 < 0 || o1 < o0 || o1 > p.n_events) {
+        if (tid == 0) atomicOr(p.err, kErrOrder);
+        o0 = o1 = 0;
+    }
+    uint32_t bad = 0;
+    if (p.vec_ok) {
+        int64_t h1 = o1 < ((o0 + 3) & ~3ll) ? o1 : ((o0 + 3) & ~3ll);
+        int64_t v1 = h1 > (o1 & ~3ll) ? h1 : (o1 & ~3ll);
+        for (int64_t i = o0 + tid; i < h1; i += nthr) bad |= scatter_event(fr, p, __ldg(p.xy + i));
+        const uint4* x4 = reinterpret_cast<const uint4*>(p.xy);
+        int64_t j = (h1 >> 2) + tid;
+        const int64_t j1 = v1 >> 2;
+        for (; j + 3 * nthr < j1; j += 4 * nthr) {   // 4 loads in flight per thread
+            uint4 q0 = ld_stream_u4(x4 + j), q1 = ld_stream_u4(x4 + j + nthr);
+            uint4 q2 = ld_stream_u4(x4 + j + 2 * nthr), q3 = ld_stream_u4(x4 + j + 3 * nthr);
+            bad |= scatter_event(fr, p, q0.x) | scatter_event(fr, p, q0.y) | scatter_event(fr, p, q0.z) | scatter_event(fr, p, q0.w);
+            bad |= scatter_event(fr, p, q1.x) | scatter_event(fr, p, q1.y) | scatter_event(fr, p, q1.z) | scatter_event(fr, p, q1.w);
+            bad |= scatter_event(fr, p, q2.x) | scatter_event(fr, p, q2.y) | scatter_event(fr, p, q2.z) | scatter_event(fr, p, q2.w);
+            bad |= scatter_event(fr, p, q3.x) | scatter_event(fr, p, q3.y) | scatter_event(fr, p, q3.z) | scatter_event(fr, p, q3.w);
+        }
+        for (; j < j1; j += nthr) {
+            uint4 q = ld_stream_u4(x4 + j);
+            bad |= scatter_event(fr, p, q.x) | scatter_event(fr, p, q.y) | scatter_event(fr, p, q.z) | scatter_event(fr, p, q.w);
+        }
+        for (int64_t i = v1 + tid; i < o1; i += nthr) bad |= scatter_event(fr, p, __ldg(p.xy + i));
+    } else {
+        for (int64_t i = o0 + tid; i < o1; i += nthr) bad |= scatter_event(fr, p, __ldg(p.xy + i));
+    }
+    if (bad) atomicOr(p.err, kErrRange);
+    __syncthreads();
+
+    if (p.E_out) {
+        uint32_t* out = p.E_out + (size_t)b * p.H * p.NW;
+        for (int i = tid; i < p.H * p.NW; i += nthr) out[i] = fr[(i / p.NW) * p.NWP + (i % p.NW)];
+    }
+
+    // ---- a2 + a3 on 32x32 blocks (lane = row), then transpose the block into T
+    const uint32_t lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : kFull;
+    const int nitems = p.NR * p.NW;
+    for (int item = warp; item < nitems; item += nwarps) {
+        const int r = item / p.NW, w = item - r * p.NW;
+        const int y = 32 * r + lane;
+        const uint32_t cd = denoised_word(fr, p, y, w);
+        const uint32_t ld = denoised_word(fr, p, y, w - 1);
+        const uint32_t rd = denoised_word(fr, p, y, w + 1);
+        const uint32_t xd = denoised_word(fr, p, lane == 0 ? 32 * r - 1 : 32 * r + 32, w);
+        uint32_t up = __shfl_up_sync(kFull, cd, 1);
+        uint32_t dn = __shfl_down_sync(kFull, cd, 1);
+        if (lane == 0) up = xd;
+        if (lane == 31) dn = xd;
+        const uint32_t lf = (cd << 1) | (ld >> 31), rt = (cd >> 1) | (rd << 31);
+        uint32_t df = cd | at_least(p.n_f, up, dn, lf, rt);
+        if (w == p.NW - 1) df &= lastmask;
+        if (y >= p.H) df = 0u;
+        if (y < p.H) {
+            const size_t o = ((size_t)b * p.H + y) * p.NW + w;
+            if (p.Ed_out) p.Ed_out[o] = cd;
+            if (p.Edf_out) p.Edf_out[o] = df;
+        }
+        const uint32_t t = warp_transpose32(df, lane);
+        const int x = 32 * w + lane;
+        if (x < p.W) {
+            p.T[((size_t)b * p.NR + r) * p.W + x] = t;
+            if (t) atomicOr(&cm[x], 1ull << r);
+        }
+    }
+    __syncthreads();
+    for (int x = tid; x < p.W; x += nthr) p.colmask[(size_t)b * p.W + x] = cm[x];
+}
+
+}  // namespace ieds

@@ -1,0 +1,443 @@
+// ieds.cu -- C ABI (include/ieds.h) of the batched IEDS build on B200 (sm_100a).
+//
+// Host side: configuration validation, scratch ownership, the fp64-built Eq. (1) table,
+// stream-ordered launches chunk by chunk, the latched device error flag, and the
+// pipelined host-buffer entry point.  Kernels: frame_kernel.cuh (a1-a3), edt_kernel.cuh
+// (a4-a5).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ieds.h"
+#include "frame_kernel.cuh"
+#include "edt_kernel.cuh"
+
+#ifndef IEDS_VERSION_STR
+#define IEDS_VERSION_STR "ieds-b200 0.1 (sm_100a)"
+#endif
+
+namespace {
+
+constexpr int kFrameThreads = 1024;
+constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
+constexpr int kLutMax = 1024;
+constexpr int kSegTarget = 80;     // columns per EDT segment (warp)
+
+struct HostPath {
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};    // chunk's copies + kernels finished
+    cudaEvent_t kdone[2] = {nullptr, nullptr};   // chunk's kernels finished (scratch free)
+    uint32_t* d_xy[2] = {nullptr, nullptr};
+    int64_t* d_off[2] = {nullptr, nullptr};
+    float* d_S[2] = {nullptr, nullptr};
+    int64_t* h_off[2] = {nullptr, nullptr};   // pinned, rebased offsets
+    int64_t cap_ev[2] = {0, 0};
+};
+
+}  // namespace
+
+struct ProfPool {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;   // pairs (start, end)
+    std::vector<int> kind;         // per pair
+    size_t used = 0;               // pairs recorded since last read
+};
+
+struct ieds_handle {
+    ieds_config cfg;
+    int dev;
+    int NW, NWP, NR, NS, SEGW;
+    int chunk;
+    size_t smem_frame, smem_edt, smem_edt_d2;
+    uint32_t* T = nullptr;
+    unsigned long long* colmask = nullptr;
+    int* err = nullptr;
+    int* h_err = nullptr;   // pinned
+    float* lut = nullptr;
+    int K_lut, K_sat;
+    float c_exp;
+    HostPath hp;
+    ProfPool prof;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+size_t edt_smem_bytes(int W, int NS, int SEGW, int K_lut, bool d2) {
+    size_t b = 8ull * W + 4ull * ((K_lut + 3) & ~3) + 2ull * 2 * 32 * NS + 4ull * 32 * 9 * NS;
+    if (d2) b += 4ull * 32 * 9 * NS;
+    b += (size_t)NS * SEGW * 32;
+    return b;
+}
+
+// fp32 value of Eq. (1) rounded from fp64, and the first D2 at which it is exactly 1.0f
+float surface_f32(double d2, double alpha) { return (float)(1.0 - std::exp(-std::sqrt(d2) / alpha)); }
+
+int64_t saturation_index(double alpha) {
+    int64_t lo = 0, hi = 1;
+    while (surface_f32((double)hi, alpha) != 1.0f) {
+        hi *= 2;
+        if (hi > (1ll << 40)) return hi;
+    }
+    while (lo < hi) {   // first D2 with value 1.0f (the value is monotone in D2)
+        int64_t mid = lo + (hi - lo) / 2;
+        if (surface_f32((double)mid, alpha) == 1.0f) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+int cuda_fail(cudaError_t e) { return e == cudaErrorMemoryAllocation ? IEDS_ENOMEM : IEDS_ECUDA; }
+
+void free_host_path(HostPath& hp) {
+    for (int i = 0; i < 2; ++i) {
+        if (hp.st[i]) cudaStreamDestroy(hp.st[i]);
+        if (hp.done[i]) cudaEventDestroy(hp.done[i]);
+        if (hp.kdone[i]) cudaEventDestroy(hp.kdone[i]);
+        cudaFree(hp.d_xy[i]);
+        cudaFree(hp.d_off[i]);
+        cudaFree(hp.d_S[i]);
+        cudaFreeHost(hp.h_off[i]);
+    }
+    hp = HostPath{};
+}
+
+// returns the event pair to record around the next launch of `kind`, or nulls
+void prof_pair(ieds_handle* h, int kind, cudaEvent_t* a, cudaEvent_t* b) {
+    *a = *b = nullptr;
+    ProfPool& p = h->prof;
+    if (!p.on) return;
+    if (p.used * 2 + 2 > p.ev.size()) {
+        cudaEvent_t e0, e1;
+        if (cudaEventCreate(&e0) != cudaSuccess) return;
+        if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); return; }
+        p.ev.push_back(e0);
+        p.ev.push_back(e1);
+        p.kind.push_back(kind);
+    }
+    p.kind[p.used] = kind;
+    *a = p.ev[2 * p.used];
+    *b = p.ev[2 * p.used + 1];
+    ++p.used;
+}
+
+int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int64_t n_events, int nb,
+                 float* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st) {
+    ieds::FrameParams fp;
+    fp.xy = xy;
+    fp.offsets = offsets;
+    fp.n_events = n_events;
+    fp.W = h->cfg.width;
+    fp.H = h->cfg.height;
+    fp.NW = h->NW;
+    fp.NWP = h->NWP;
+    fp.NR = h->NR;
+    fp.n_d = h->cfg.n_d;
+    fp.n_f = h->cfg.n_f;
+    fp.vec_ok = ((reinterpret_cast<uintptr_t>(xy) & 15u) == 0) ? 1 : 0;
+    fp.T = h->T;
+    fp.colmask = h->colmask;
+    fp.E_out = E;
+    fp.Ed_out = Ed;
+    fp.Edf_out = Edf;
+    fp.err = h->err;
+    cudaEvent_t pa, pb;
+    prof_pair(h, 0, &pa, &pb);
+    if (pa) cudaEventRecord(pa, st);
+    ieds::frame_kernel<<<nb, kFrameThreads, h->smem_frame, st>>>(fp);
+    if (pb) cudaEventRecord(pb, st);
+
+    ieds::EdtParams ep;
+    ep.T = h->T;
+    ep.colmask = h->colmask;
+    ep.W = h->cfg.width;
+    ep.H = h->cfg.height;
+    ep.NR = h->NR;
+    ep.NS = h->NS;
+    ep.SEGW = h->SEGW;
+    ep.S = S;
+    ep.D2 = D2;
+    ep.lut = h->lut;
+    ep.K_lut = h->K_lut;
+    ep.K_sat = h->K_sat;
+    ep.c_exp = h->c_exp;
+    dim3 grid(h->NR, nb);
+    prof_pair(h, 1, &pa, &pb);
+    if (pa) cudaEventRecord(pa, st);
+    ieds::edt_kernel<<<grid, h->NS * 32, D2 ? h->smem_edt_d2 : h->smem_edt, st>>>(ep);
+    if (pb) cudaEventRecord(pb, st);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ieds_version(void) { return IEDS_VERSION_STR; }
+
+const char* ieds_strerror(int code) {
+    switch (code) {
+        case IEDS_OK: return "ok";
+        case IEDS_EINVAL: return "invalid argument";
+        case IEDS_ERANGE: return "event outside the frame";
+        case IEDS_ECAPACITY: return "capacity exceeded";
+        case IEDS_EORDER: return "window offsets not non-decreasing or out of range";
+        case IEDS_ECUDA: return "CUDA error";
+        case IEDS_ENOMEM: return "out of memory";
+        default: return "unknown error";
+    }
+}
+
+double ieds_alpha_from_dsat(double d_sat) {
+    if (!(d_sat > 0.0) || !std::isfinite(d_sat)) return NAN;
+    return d_sat / std::log(255.0);   // -d_sat / ln(1/255), Eq. (2)-(3)
+}
+
+int ieds_create(const ieds_config* cfg, ieds_handle** out) {
+    if (!out) return IEDS_EINVAL;
+    *out = nullptr;
+    if (!cfg) return IEDS_EINVAL;
+    const int W = cfg->width, H = cfg->height;
+    if (W < 1 || W > 4096 || H < 1 || H > 2048) return IEDS_EINVAL;
+    if (cfg->n_d < 0 || cfg->n_d > 4 || cfg->n_f < 1 || cfg->n_f > 5) return IEDS_EINVAL;
+    if (!(cfg->alpha > 0.0) || !std::isfinite(cfg->alpha)) return IEDS_EINVAL;
+    if (cfg->chunk_windows < 0) return IEDS_EINVAL;
+
+    ieds_handle* h = new ieds_handle();
+    h->cfg = *cfg;
+    int dev = cfg->device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+        delete h;
+        return IEDS_ECUDA;
+    }
+    h->dev = dev;
+    DeviceGuard g(dev);
+    if (!g.ok) {
+        delete h;
+        return IEDS_ECUDA;
+    }
+    h->NW = (W + 31) / 32;
+    h->NWP = h->NW | 1;
+    h->NR = (H + 31) / 32;
+    int ns = (W + kSegTarget - 1) / kSegTarget;
+    ns = std::max(1, std::min(16, ns));
+    int segw = ((W + ns - 1) / ns + 7) & ~7;
+    ns = (W + segw - 1) / segw;
+    h->NS = ns;
+    h->SEGW = segw;
+
+    const double alpha = cfg->alpha;
+    int64_t ksat = saturation_index(alpha);
+    if (ksat > (1ll << 31)) ksat = (1ll << 31);
+    h->K_sat = (int)std::min<int64_t>(ksat, 0x7FFFFFFF);
+    h->K_lut = (int)std::min<int64_t>(ksat, kLutMax);
+    h->c_exp = (float)(-1.0 / (alpha * std::log(2.0)));
+
+    h->smem_frame = 4ull * ((h->NWP * H + 3) & ~3) + 8ull * W;
+    h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
+    h->smem_edt_d2 = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, true);
+    if (h->smem_frame > (size_t)kMaxSmem || h->smem_edt_d2 > (size_t)kMaxSmem || h->SEGW > 255) {
+        delete h;
+        return IEDS_EINVAL;
+    }
+
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    h->chunk = cfg->chunk_windows > 0 ? cfg->chunk_windows : 2 * nsm;
+
+    cudaError_t e;
+    e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
+    if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
+    if (e == cudaSuccess) e = cudaMalloc(&h->colmask, sizeof(unsigned long long) * (size_t)h->chunk * W);
+    if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMallocHost(&h->h_err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&h->lut, sizeof(float) * std::max(1, h->K_lut));
+    if (e == cudaSuccess) {
+        std::vector<float> lut(std::max(1, h->K_lut));
+        for (int i = 0; i < h->K_lut; ++i) lut[i] = surface_f32((double)i, alpha);
+        e = cudaMemcpy(h->lut, lut.data(), sizeof(float) * lut.size(), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {
+        int rc = cuda_fail(e);
+        cudaGetLastError();
+        ieds_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return IEDS_OK;
+}
+
+void ieds_destroy(ieds_handle* h) {
+    if (!h) return;
+    DeviceGuard g(h->dev);
+    cudaDeviceSynchronize();
+    free_host_path(h->hp);
+    for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
+    cudaFree(h->T);
+    cudaFree(h->colmask);
+    cudaFree(h->err);
+    cudaFree(h->lut);
+    cudaFreeHost(h->h_err);
+    delete h;
+}
+
+int ieds_profile_enable(ieds_handle* h, int on) {
+    if (!h) return IEDS_EINVAL;
+    h->prof.on = on != 0;
+    return IEDS_OK;
+}
+
+int ieds_profile_read(ieds_handle* h, double* frame_ms, int64_t* frame_launches, double* edt_ms,
+                      int64_t* edt_launches) {
+    if (!h) return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    double ms[2] = {0.0, 0.0};
+    int64_t n[2] = {0, 0};
+    ProfPool& p = h->prof;
+    for (size_t i = 0; i < p.used; ++i) {
+        if (cudaEventSynchronize(p.ev[2 * i + 1]) != cudaSuccess) return IEDS_ECUDA;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, p.ev[2 * i], p.ev[2 * i + 1]) != cudaSuccess) return IEDS_ECUDA;
+        ms[p.kind[i]] += t;
+        n[p.kind[i]] += 1;
+    }
+    p.used = 0;
+    if (frame_ms) *frame_ms = ms[0];
+    if (frame_launches) *frame_launches = n[0];
+    if (edt_ms) *edt_ms = ms[1];
+    if (edt_launches) *edt_launches = n[1];
+    return IEDS_OK;
+}
+
+int64_t ieds_launches_per_batch(const ieds_handle* h, int32_t num_windows) {
+    if (!h || num_windows <= 0) return 0;
+    return 2ll * ((num_windows + h->chunk - 1) / h->chunk);
+}
+
+int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* window_offsets,
+                     int64_t n_events, int32_t num_windows, float* surfaces, uint32_t* edge_bits,
+                     uint32_t* denoised_bits, uint32_t* filtered_bits, uint32_t* sqdist, void* stream) {
+    if (!h || num_windows < 0 || n_events < 0) return IEDS_EINVAL;
+    if (num_windows == 0) return IEDS_OK;
+    if (!surfaces || !window_offsets || (n_events > 0 && !events_xy)) return IEDS_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(events_xy) & 3u) || (reinterpret_cast<uintptr_t>(surfaces) & 3u))
+        return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t plane = (size_t)h->cfg.width * h->cfg.height;
+    const size_t bplane = (size_t)h->NW * h->cfg.height;
+    for (int c0 = 0; c0 < num_windows; c0 += h->chunk) {
+        const int nb = std::min(h->chunk, num_windows - c0);
+        int rc = launch_chunk(h, events_xy, window_offsets + c0, n_events, nb, surfaces + c0 * plane,
+                              edge_bits ? edge_bits + c0 * bplane : nullptr,
+                              denoised_bits ? denoised_bits + c0 * bplane : nullptr,
+                              filtered_bits ? filtered_bits + c0 * bplane : nullptr,
+                              sqdist ? sqdist + c0 * plane : nullptr, st);
+        if (rc != IEDS_OK) return rc;
+    }
+    return IEDS_OK;
+}
+
+int ieds_sync(ieds_handle* h, void* stream) {
+    if (!h) return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(h->h_err, h->err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->err, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return IEDS_ECUDA;
+    const int f = *h->h_err;
+    if (f & ieds::kErrOrder) return IEDS_EORDER;
+    if (f & ieds::kErrRange) return IEDS_ERANGE;
+    return IEDS_OK;
+}
+
+int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64_t* window_offsets,
+                          int32_t num_windows, float* surfaces) {
+    if (!h || num_windows < 0) return IEDS_EINVAL;
+    if (num_windows == 0) return IEDS_OK;
+    if (!window_offsets || !surfaces) return IEDS_EINVAL;
+    for (int32_t b = 0; b < num_windows; ++b)
+        if (window_offsets[b + 1] < window_offsets[b] || window_offsets[b] < 0) return IEDS_EORDER;
+    if (window_offsets[num_windows] > window_offsets[0] && !events_xy) return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    HostPath& hp = h->hp;
+    cudaError_t e = cudaSuccess;
+    const size_t plane = (size_t)h->cfg.width * h->cfg.height;
+    const int chunk = h->chunk;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        if (!hp.st[i]) e = cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess && !hp.done[i]) e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming);
+        if (e == cudaSuccess && !hp.kdone[i]) e = cudaEventCreateWithFlags(&hp.kdone[i], cudaEventDisableTiming);
+        if (e == cudaSuccess && !hp.d_S[i]) e = cudaMalloc(&hp.d_S[i], sizeof(float) * plane * chunk);
+        if (e == cudaSuccess && !hp.d_off[i]) e = cudaMalloc(&hp.d_off[i], sizeof(int64_t) * (chunk + 1));
+        if (e == cudaSuccess && !hp.h_off[i]) e = cudaMallocHost(&hp.h_off[i], sizeof(int64_t) * (chunk + 1));
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    // The two internal streams alternate chunks; the scratch (T, colmask) is shared, so the
+    // kernels of consecutive chunks are ordered through events while copies overlap.
+    int rc = IEDS_OK;
+    int k = 0;
+    for (int c0 = 0; c0 < num_windows; c0 += chunk, k ^= 1) {
+        const int nb = std::min(chunk, num_windows - c0);
+        const int64_t e0 = window_offsets[c0], e1 = window_offsets[c0 + nb];
+        const int64_t nev = e1 - e0;
+        cudaStream_t st = hp.st[k];
+        // buffer k was last used two chunks ago: wait until its copies/kernels finished
+        e = cudaEventSynchronize(hp.done[k]);
+        if (e == cudaSuccess && nev > hp.cap_ev[k]) {
+            cudaFree(hp.d_xy[k]);
+            hp.d_xy[k] = nullptr;
+            hp.cap_ev[k] = 0;
+            e = cudaMalloc(&hp.d_xy[k], sizeof(uint32_t) * (size_t)std::max<int64_t>(nev, 4));
+            if (e == cudaSuccess) hp.cap_ev[k] = nev;
+        }
+        if (e != cudaSuccess) return cuda_fail(e);
+        for (int b = 0; b <= nb; ++b) hp.h_off[k][b] = window_offsets[c0 + b] - e0;
+        if (nev > 0)
+            e = cudaMemcpyAsync(hp.d_xy[k], events_xy + e0, sizeof(uint32_t) * nev, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hp.d_off[k], hp.h_off[k], sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) {
+            // order the kernels after the previous chunk's kernels (shared scratch)
+            e = cudaStreamWaitEvent(st, hp.kdone[k ^ 1], 0);
+        }
+        if (e != cudaSuccess) return cuda_fail(e);
+        rc = launch_chunk(h, hp.d_xy[k], hp.d_off[k], nev, nb, hp.d_S[k], nullptr, nullptr, nullptr, nullptr, st);
+        if (rc != IEDS_OK) return rc;
+        e = cudaEventRecord(hp.kdone[k], st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        e = cudaMemcpyAsync(surfaces + (size_t)c0 * plane, hp.d_S[k], sizeof(float) * plane * nb,
+                            cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(hp.done[k], st);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    e = cudaStreamSynchronize(hp.st[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(hp.st[1]);
+    if (e != cudaSuccess) return IEDS_ECUDA;
+    return ieds_sync(h, hp.st[0]);
+}
+
+}  // extern "C"

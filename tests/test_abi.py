@@ -1,0 +1,84 @@
+"""CPU-side checks of the C ABI: the in-tree library builds/loads and exports every symbol that
+include/ieds.h declares; host-only entry points behave (no compute calls without a GPU)."""
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2112_10591_b200 import _lib
+
+    return _lib.load()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "ieds.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ieds_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declarations_match_binding():
+    from paper_2112_10591_b200 import _lib
+
+    assert declared_functions() == sorted(_lib.EXPORTS)
+
+
+def test_every_declared_symbol_exported(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+        assert ctypes.cast(getattr(lib, name), ctypes.c_void_p).value
+
+
+def test_host_only_entry_points(lib):
+    assert lib.ieds_version().decode().startswith("ieds-b200")
+    assert lib.ieds_strerror(0) == b"ok"
+    assert lib.ieds_strerror(-2) == b"event outside the frame"
+    # Eq. (2)-(3): alpha = d_sat / ln 255 ~ d_sat / 5.541, 1.08 for 6 px
+    a6 = lib.ieds_alpha_from_dsat(6.0)
+    assert abs(a6 - 1.08) < 5e-3 and abs(6.0 / a6 - 5.541) < 5e-4
+    assert abs(lib.ieds_alpha_from_dsat(math.log(255.0)) - 1.0) < 1e-15
+    assert math.isnan(lib.ieds_alpha_from_dsat(0.0)) and math.isnan(lib.ieds_alpha_from_dsat(-3.0))
+
+
+def test_create_rejects_bad_config_before_touching_cuda(lib):
+    from paper_2112_10591_b200._lib import IEDS_EINVAL, IedsConfig
+
+    h = ctypes.c_void_p()
+    for cfg in [IedsConfig(0, 10, 1, 4, 1.0, 0, 0), IedsConfig(10, 10, 5, 4, 1.0, 0, 0),
+                IedsConfig(10, 10, 1, 0, 1.0, 0, 0), IedsConfig(10, 10, 1, 4, float("nan"), 0, 0),
+                IedsConfig(10, 10, 1, 4, -2.0, 0, 0), IedsConfig(10, 3000, 1, 4, 1.0, 0, 0)]:
+        assert lib.ieds_create(ctypes.byref(cfg), ctypes.byref(h)) == IEDS_EINVAL
+        assert not h.value
+    assert lib.ieds_create(None, ctypes.byref(h)) == IEDS_EINVAL
+    lib.ieds_destroy(None)   # NULL-safe
+
+
+def test_build_batch_argument_errors_without_handle(lib):
+    from paper_2112_10591_b200._lib import IEDS_EINVAL
+
+    assert lib.ieds_build_batch(None, None, None, 0, 1, None, None, None, None, None, None) == IEDS_EINVAL
+    assert lib.ieds_sync(None, None) == IEDS_EINVAL
+    assert lib.ieds_launches_per_batch(None, 10) == 0
+
+
+def test_sass_is_sm100a(lib):
+    """The library carries sm_100a SASS (cuobjdump), built with nvcc here."""
+    import shutil
+    import subprocess
+
+    from paper_2112_10591_b200._lib import LIB_PATH
+
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

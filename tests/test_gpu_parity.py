@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Bar (BASELINE.json north_star): E, E_d, E_df bit-exact; D2 exact (integer); surface within
+max-abs 2e-6 of the oracle's fp64 values.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth.events import (WORKLOADS, SceneConfig, batch_events, pack_xy, pattern_events,
+                          random_frame_events)
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-6
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def ieds():
+    import paper_2112_10591_b200 as m
+    return m
+
+
+def unpack(bits, W, H):
+    nw = (W + 31) // 32
+    a = np.ascontiguousarray(bits).view(np.uint32).reshape(H, nw)
+    full = np.unpackbits(a.view(np.uint8), bitorder="little").reshape(H, nw * 32)
+    assert not full[:, W:].any(), "padding bits must stay 0"
+    return full[:, :W]
+
+
+def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True):
+    torch = _torch()
+    dev = torch.device("cuda", 0)
+    B = len(off) - 1
+    nw = (W + 31) // 32
+    base = torch.zeros(len(xy) + xy_shift + 4, dtype=torch.int32, device=dev)
+    if len(xy):
+        base[xy_shift:xy_shift + len(xy)] = torch.from_numpy(np.ascontiguousarray(xy).view(np.int32)).to(dev)
+    txy = base[xy_shift:xy_shift + len(xy)]
+    toff = torch.from_numpy(np.asarray(off, np.int64)).to(dev)
+    outs = {}
+    if debug:
+        for k in ("E", "E_d", "E_df"):
+            outs[k] = torch.full((B, H, nw), -1, dtype=torch.int32, device=dev)
+        outs["D2"] = torch.full((B, H, W), 7, dtype=torch.int32, device=dev)
+    S = torch.full((B, H, W), -5.0, dtype=torch.float32, device=dev)
+    with ieds().Builder(W, H, n_d, n_f, alpha=alpha, chunk_windows=chunk, device=0) as bld:
+        bld.build_batch(txy, toff, S, edge_bits=outs.get("E"), denoised_bits=outs.get("E_d"),
+                        filtered_bits=outs.get("E_df"), sqdist=outs.get("D2"))
+        bld.sync()
+    res = {"S": S.cpu().numpy()}
+    for k, v in outs.items():
+        res[k] = v.cpu().numpy().view(np.uint32)
+    return res
+
+
+def check_window(gpu, b, xy_w, W, H, n_d, n_f, alpha, debug=True):
+    ref = oracle.build_window(xy_w, W, H, n_d, n_f, alpha)
+    if debug:
+        for k in ("E", "E_d", "E_df"):
+            got = unpack(gpu[k][b], W, H)
+            assert np.array_equal(got, ref[k]), (k, b, int((got != ref[k]).sum()))
+        ref_d2 = np.where(ref["D2"] < 0, 0xFFFFFFFF, ref["D2"]).astype(np.uint32)
+        bad = gpu["D2"][b] != ref_d2
+        assert not bad.any(), ("D2", b, int(bad.sum()), np.argwhere(bad)[:5])
+    err = np.abs(gpu["S"][b].astype(np.float64) - ref["S"])
+    assert err.max() <= TOL, ("S", b, float(err.max()))
+    # exact structure: 0 exactly on E_df pixels, 1.0 exactly for empty frames
+    assert np.all((gpu["S"][b] == 0) == (ref["E_df"] == 1))
+    return ref
+
+
+def csr(windows):
+    off = np.zeros(len(windows) + 1, np.int64)
+    off[1:] = np.cumsum([len(w) for w in windows])
+    xy = np.concatenate(windows).astype(np.uint32) if windows else np.zeros(0, np.uint32)
+    return xy, off
+
+
+# ----------------------------------------------------------------------------- configs
+
+@pytest.mark.parametrize("name,nwin", [("C1", 1), ("C2", 24), ("C3", 6), ("C5", 3)])
+def test_parity_workload_configs(name, nwin):
+    wl = WORKLOADS[name]
+    c = wl.scene
+    alpha = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 0, nwin)
+    gpu = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, alpha)
+    for b in range(nwin):
+        check_window(gpu, b, xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, alpha)
+
+
+def test_parity_alpha_printed_value():
+    # the paper prints alpha = 1.08; parity must hold for that exact value too
+    wl = WORKLOADS["C1"]
+    c = wl.scene
+    xy, off = batch_events(c, wl.seed, 5, 2)
+    gpu = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, 1.08)
+    for b in range(2):
+        check_window(gpu, b, xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, 1.08)
+
+
+# ----------------------------------------------------------------------------- edge cases
+
+@pytest.mark.parametrize("W,H", [(1, 1), (1, 40), (37, 1), (33, 17), (64, 64), (346, 260), (100, 70)])
+def test_parity_patterns_and_sizes(W, H):
+    wins = [pattern_events(W, H, p, seed=i) for i, p in
+            enumerate(["empty", "single", "all", "checker", "row", "col", "corners"])]
+    for i, d in enumerate([0.001, 0.01, 0.1, 0.3, 0.5]):
+        wins.append(random_frame_events(W, H, d, seed=100 + i))
+    xy, off = csr(wins)
+    for n_d, n_f in [(0, 5), (0, 2), (1, 4), (2, 3)]:
+        gpu = run_gpu(xy, off, W, H, n_d, n_f, 1.0827855)
+        for b in range(len(wins)):
+            check_window(gpu, b, xy[off[b]:off[b + 1]], W, H, n_d, n_f, 1.0827855)
+
+
+def test_parity_isolated_event_closed_form():
+    # single event, N_d = 0, N_f = 2: S(x,y) = 1 - exp(-|(x,y)-(x0,y0)|/alpha)  (Eq. (1))
+    W, H, x0, y0 = 300, 200, 123, 77
+    alpha = oracle.alpha_from_dsat(6.0)
+    xy, off = csr([pack_xy([x0], [y0])])
+    gpu = run_gpu(xy, off, W, H, 0, 2, alpha)
+    yy, xx = np.mgrid[0:H, 0:W]
+    exp = 1.0 - np.exp(-np.hypot(xx - x0, yy - y0) / alpha)
+    assert np.abs(gpu["S"][0] - exp).max() <= TOL
+    assert gpu["D2"][0][y0, x0] == 0 and gpu["D2"][0][0, 0] == x0 * x0 + y0 * y0
+
+
+def test_parity_max_distance_corners():
+    # two far corner points: maximal D2 = (W-1)^2 + (H-1)^2 is reached at the far corners
+    W, H = 1280, 720
+    xy, off = csr([pack_xy([0], [0])])
+    gpu = run_gpu(xy, off, W, H, 0, 5, 2.0)
+    assert gpu["D2"][0][H - 1, W - 1] == (W - 1) ** 2 + (H - 1) ** 2
+    check_window(gpu, 0, xy, W, H, 0, 5, 2.0)
+
+
+def test_parity_parameter_grid():
+    # sensitivity grid of Fig. 9: N_d 0-4, N_f 1-5, d_sat 3/6/9/12
+    W, H = 83, 61
+    wins = [random_frame_events(W, H, d, seed=200 + i) for i, d in enumerate([0.02, 0.15, 0.4])]
+    xy, off = csr(wins)
+    for n_d in range(5):
+        for n_f in range(1, 6):
+            for d_sat in (3.0, 6.0, 9.0, 12.0):
+                a = oracle.alpha_from_dsat(d_sat)
+                gpu = run_gpu(xy, off, W, H, n_d, n_f, a)
+                for b in range(len(wins)):
+                    check_window(gpu, b, xy[off[b]:off[b + 1]], W, H, n_d, n_f, a)
+
+
+def test_parity_large_alpha_mufu_path():
+    # alpha large enough that the saturation index exceeds the 1024-entry table
+    W, H = 200, 150
+    xy, off = csr([random_frame_events(W, H, 0.002, seed=9)])
+    for a in (10.0, 40.0):
+        gpu = run_gpu(xy, off, W, H, 0, 5, a)
+        check_window(gpu, 0, xy, W, H, 0, 5, a)
+
+
+# ----------------------------------------------------------------------------- batching
+
+def test_chunking_and_ragged_windows_identical():
+    cfg = SceneConfig(346, 260, 20_000, n_prims=28, len_range=(15.0, 120.0), sigma=0.45,
+                      count_jitter=0.9)
+    xy, off = batch_events(cfg, 77, 0, 11)
+    # insert empty windows
+    off = np.concatenate([off[:3], [off[2]], off[3:7], [off[6], off[6]], off[7:]])
+    a = oracle.alpha_from_dsat(6.0)
+    g1 = run_gpu(xy, off, 346, 260, 1, 4, a, chunk=0)
+    g2 = run_gpu(xy, off, 346, 260, 1, 4, a, chunk=3, xy_shift=1)   # unaligned events, 5 chunks
+    for k in g1:
+        assert np.array_equal(g1[k], g2[k]), k
+    for b in range(len(off) - 1):
+        check_window(g1, b, xy[off[b]:off[b + 1]], 346, 260, 1, 4, a)
+
+
+def test_surface_only_path_matches_debug_path():
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 10, 4)
+    g1 = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, a, debug=True)
+    g2 = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, a, debug=False)
+    assert np.array_equal(g1["S"], g2["S"])
+
+
+def test_host_entry_point_matches_device():
+    wl = WORKLOADS["C1"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 0, 9)
+    g = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, a, debug=False)
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, chunk_windows=4, device=0) as bld:
+        S = bld.build_batch_host(xy, off)
+    assert np.array_equal(S, g["S"])
+
+
+# ----------------------------------------------------------------------------- errors
+
+def test_out_of_frame_event_latched_and_dropped():
+    torch = _torch()
+    ie = ieds()
+    W, H = 64, 32
+    good = random_frame_events(W, H, 0.2, seed=1)
+    bad = np.concatenate([good, pack_xy([W], [0]), pack_xy([0], [H])])
+    xy, off = csr([bad])
+    dev = torch.device("cuda", 0)
+    with ie.Builder(W, H, 0, 5, alpha=1.0, device=0) as bld:
+        S = bld.build_batch(torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev))
+        with pytest.raises(ie.IedsRangeError):
+            bld.sync()
+        bld.sync()   # cleared
+        ref = oracle.build_window(good, W, H, 0, 5, 1.0)
+        assert np.abs(S.cpu().numpy()[0] - ref["S"]).max() <= TOL
+        off_bad = torch.tensor([0, 5, 3], dtype=torch.int64, device=dev)
+        bld.build_batch(torch.from_numpy(xy.view(np.int32)).to(dev), off_bad)
+        with pytest.raises(ie.IedsOrderError):
+            bld.sync()
+
+
+def test_invalid_configs_rejected():
+    ie = ieds()
+    for args in [(0, 10, 1, 4), (10, 0, 1, 4), (10, 10, 5, 4), (10, 10, 1, 0), (10, 10, 1, 6),
+                 (5000, 10, 1, 4), (10, 5000, 1, 4)]:
+        with pytest.raises(ie.IedsError):
+            ie.Builder(*args, alpha=1.0, device=0)
+    with pytest.raises(ie.IedsError):
+        ie.Builder(10, 10, 1, 4, alpha=-1.0, device=0)
+
+
+# ----------------------------------------------------------------------------- full size
+
+def test_full_size_bench_config_sampled():
+    """C3 at its full BASELINE size (1000 windows) in the bench launch configuration; a
+    sample of windows across all chunks is checked against the oracle one by one."""
+    torch = _torch()
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 0, wl.n_windows)
+    dev = torch.device("cuda", 0)
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0) as bld:
+        S = bld.build_batch(torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev))
+        bld.sync()
+    sample = [0, 1, 147, 148, 295, 296, 511, 700, 888, 999]
+    Sh = S[sample].cpu().numpy()
+    refs = oracle.build_batch(xy, off, c.width, c.height, wl.n_d, wl.n_f, a, windows=sample,
+                              want=("S", "E_df"))
+    for i, b in enumerate(sample):
+        err = np.abs(Sh[i].astype(np.float64) - refs[i]["S"]).max()
+        assert err <= TOL, (b, err)
+        assert np.all((Sh[i] == 0) == (refs[i]["E_df"] == 1))
