@@ -70,7 +70,14 @@ typedef struct {
     int32_t chunk_windows;  /* windows processed per launch pair (sizes the scratch);    */
                             /* batches of any size are processed chunk by chunk. 0 = 128 */
     int32_t device;         /* CUDA device ordinal; -1 = current device                 */
+    int32_t flags;          /* IEDS_FLAG_* bits                                          */
 } ieds_config;
+
+/* Always run the uncapped exact-EDT kernel.  By default, when sqdist is not requested and
+ * the saturation radius c = ceil(sqrt(K_sat)) is <= 31 pixels, the surface is produced by
+ * the saturation-aware streaming kernel, which evaluates D2 exactly wherever D2 < K_sat and
+ * gives bit-identical surfaces (K_sat = first D2 whose fp32 Eq. (1) value is 1.0f). */
+#define IEDS_FLAG_EXACT_EDT 1
 
 /* Validates cfg, allocates the scratch on cfg->device and builds the Eq. (1) table.
  * On success *out is a new handle; on failure *out is NULL. */

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 
-from ._lib import (IEDS_NO_EDGE, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
+from ._lib import (IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
                    check, load)
 
 __all__ = ["Builder", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
@@ -45,12 +45,13 @@ class Builder:
     """One ieds_handle on one CUDA device.
 
     Builder(width, height, n_d, n_f, alpha=None, d_sat=6.0) -- alpha defaults to
-    alpha_from_dsat(d_sat).  build_batch() enqueues on the current torch stream (or the
+    alpha_from_dsat(d_sat).  exact_edt=True forces the uncapped exact-EDT kernel even when
+    only surfaces are requested (the default streaming kernel gives bit-identical surfaces).  build_batch() enqueues on the current torch stream (or the
     given one) and does not synchronise; sync() reports latched device errors.
     """
 
     def __init__(self, width: int, height: int, n_d: int, n_f: int, alpha: float | None = None,
-                 d_sat: float = 6.0, chunk_windows: int = 0, device=None):
+                 d_sat: float = 6.0, chunk_windows: int = 0, device=None, exact_edt: bool = False):
         import torch
 
         if not torch.cuda.is_available():
@@ -61,7 +62,9 @@ class Builder:
         if alpha is None:
             alpha = alpha_from_dsat(d_sat)
         self.params = Params(width, height, n_d, n_f, float(alpha))
-        cfg = IedsConfig(width, height, n_d, n_f, float(alpha), chunk_windows, self.device.index)
+        cfg = IedsConfig(width, height, n_d, n_f, float(alpha), chunk_windows, self.device.index,
+                         IEDS_FLAG_EXACT_EDT if exact_edt else 0)
+        self.exact_edt = exact_edt
         h = ctypes.c_void_p()
         check(load().ieds_create(ctypes.byref(cfg), ctypes.byref(h)), "ieds_create")
         self._h = h

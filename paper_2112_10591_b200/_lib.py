@@ -37,7 +37,11 @@ class IedsConfig(ctypes.Structure):
         ("alpha", ctypes.c_double),
         ("chunk_windows", ctypes.c_int32),
         ("device", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
+
+
+IEDS_FLAG_EXACT_EDT = 1
 
 
 class IedsError(RuntimeError):

@@ -29,6 +29,7 @@ struct FrameParams {
     uint32_t* __restrict__ E_out;           // [nb][H][NW] or null
     uint32_t* __restrict__ Ed_out;
     uint32_t* __restrict__ Edf_out;
+    uint32_t* __restrict__ Edf_scratch;     // [nb][H][NW] E_df for the streaming surface kernel
     int* __restrict__ err;
 };
 
@@ -170,7 +171,9 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
             const size_t o = ((size_t)b * p.H + y) * p.NW + w;
             if (p.Ed_out) p.Ed_out[o] = cd;
             if (p.Edf_out) p.Edf_out[o] = df;
+            if (p.Edf_scratch) p.Edf_scratch[o] = df;
         }
+        if (!p.T) continue;   // streaming surface kernel reads row-major E_df instead
         const uint32_t t = warp_transpose32(df, lane);
         const int x = 32 * w + lane;
         if (x < p.W) {
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
             if (t) atomicOr(&cm[x], 1ull << r);
         }
     }
+    if (!p.T) return;
     __syncthreads();
     for (int x = tid; x < p.W; x += nthr) p.colmask[(size_t)b * p.W + x] = cm[x];
 }

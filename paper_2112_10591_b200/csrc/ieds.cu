@@ -16,6 +16,7 @@
 #include "../../include/ieds.h"
 #include "frame_kernel.cuh"
 #include "edt_kernel.cuh"
+#include "surface_kernel.cuh"
 
 #ifndef IEDS_VERSION_STR
 #define IEDS_VERSION_STR "ieds-b200 0.1 (sm_100a)"
@@ -54,7 +55,9 @@ struct ieds_handle {
     int NW, NWP, NR, NS, SEGW;
     int chunk;
     size_t smem_frame, smem_edt, smem_edt_d2;
-    uint32_t* T = nullptr;
+    int c_sat;                 // ceil(sqrt(K_sat)): rows/columns a near site can be away
+    bool streaming;            // saturation-aware streaming surface kernel usable (c_sat <= 31)
+    uint32_t* T = nullptr;     // exact path: [chunk][NR][W]; streaming path: [chunk][H][NW] E_df
     unsigned long long* colmask = nullptr;
     int* err = nullptr;
     int* h_err = nullptr;   // pinned
@@ -156,12 +159,40 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     fp.E_out = E;
     fp.Ed_out = Ed;
     fp.Edf_out = Edf;
+    fp.Edf_scratch = nullptr;
     fp.err = h->err;
+    const bool stream_path = h->streaming && D2 == nullptr;
+    if (stream_path) {
+        fp.T = nullptr;
+        fp.colmask = nullptr;
+        fp.Edf_scratch = h->T;
+    }
     cudaEvent_t pa, pb;
     prof_pair(h, 0, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
     ieds::frame_kernel<<<nb, kFrameThreads, h->smem_frame, st>>>(fp);
     if (pb) cudaEventRecord(pb, st);
+
+    if (stream_path) {
+        ieds::SurfParams sp;
+        sp.Edf = h->T;
+        sp.S = S;
+        sp.lut = h->lut;
+        sp.W = h->cfg.width;
+        sp.H = h->cfg.height;
+        sp.NW = h->NW;
+        sp.K_lut = h->K_lut;
+        sp.K_sat = h->K_sat;
+        sp.c = h->c_sat;
+        sp.c_exp = h->c_exp;
+        dim3 sgrid((h->NW + ieds::kSurfWarps - 1) / ieds::kSurfWarps, nb);
+        prof_pair(h, 1, &pa, &pb);
+        if (pa) cudaEventRecord(pa, st);
+        ieds::surface_kernel<<<sgrid, ieds::kSurfWarps * 32, 0, st>>>(sp);
+        if (pb) cudaEventRecord(pb, st);
+        cudaError_t e2 = cudaGetLastError();
+        return e2 == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
+    }
 
     ieds::EdtParams ep;
     ep.T = h->T;
@@ -218,7 +249,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (W < 1 || W > 4096 || H < 1 || H > 2048) return IEDS_EINVAL;
     if (cfg->n_d < 0 || cfg->n_d > 4 || cfg->n_f < 1 || cfg->n_f > 5) return IEDS_EINVAL;
     if (!(cfg->alpha > 0.0) || !std::isfinite(cfg->alpha)) return IEDS_EINVAL;
-    if (cfg->chunk_windows < 0) return IEDS_EINVAL;
+    if (cfg->chunk_windows < 0 || (cfg->flags & ~IEDS_FLAG_EXACT_EDT)) return IEDS_EINVAL;
 
     ieds_handle* h = new ieds_handle();
     h->cfg = *cfg;
@@ -249,6 +280,14 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->K_sat = (int)std::min<int64_t>(ksat, 0x7FFFFFFF);
     h->K_lut = (int)std::min<int64_t>(ksat, kLutMax);
     h->c_exp = (float)(-1.0 / (alpha * std::log(2.0)));
+    {
+        int64_t cs = (int64_t)std::ceil(std::sqrt((double)ksat));
+        while (cs * cs < ksat) ++cs;
+        while (cs > 1 && (cs - 1) * (cs - 1) >= ksat) --cs;
+        h->c_sat = (int)std::min<int64_t>(cs, 1 << 20);
+    }
+    h->streaming = h->c_sat <= 31 && h->K_lut >= h->K_sat && H <= 2047 &&
+                   !(cfg->flags & IEDS_FLAG_EXACT_EDT);
 
     h->smem_frame = 4ull * ((h->NWP * H + 3) & ~3) + 8ull * W;
     h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
@@ -266,7 +305,9 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
-    if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
+    if (e == cudaSuccess)
+        e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk *
+                                  std::max<size_t>((size_t)h->NR * W, (size_t)h->NW * H));
     if (e == cudaSuccess) e = cudaMalloc(&h->colmask, sizeof(unsigned long long) * (size_t)h->chunk * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(int));

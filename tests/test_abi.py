@@ -53,9 +53,9 @@ def test_create_rejects_bad_config_before_touching_cuda(lib):
     from paper_2112_10591_b200._lib import IEDS_EINVAL, IedsConfig
 
     h = ctypes.c_void_p()
-    for cfg in [IedsConfig(0, 10, 1, 4, 1.0, 0, 0), IedsConfig(10, 10, 5, 4, 1.0, 0, 0),
-                IedsConfig(10, 10, 1, 0, 1.0, 0, 0), IedsConfig(10, 10, 1, 4, float("nan"), 0, 0),
-                IedsConfig(10, 10, 1, 4, -2.0, 0, 0), IedsConfig(10, 3000, 1, 4, 1.0, 0, 0)]:
+    for cfg in [IedsConfig(0, 10, 1, 4, 1.0, 0, 0, 0), IedsConfig(10, 10, 5, 4, 1.0, 0, 0, 0),
+                IedsConfig(10, 10, 1, 0, 1.0, 0, 0, 0), IedsConfig(10, 10, 1, 4, float("nan"), 0, 0, 0),
+                IedsConfig(10, 10, 1, 4, -2.0, 0, 0, 0), IedsConfig(10, 3000, 1, 4, 1.0, 0, 0, 0), IedsConfig(10, 10, 1, 4, 1.0, 0, 0, 8)]:
         assert lib.ieds_create(ctypes.byref(cfg), ctypes.byref(h)) == IEDS_EINVAL
         assert not h.value
     assert lib.ieds_create(None, ctypes.byref(h)) == IEDS_EINVAL

@@ -32,7 +32,10 @@ def unpack(bits, W, H):
     return full[:, :W]
 
 
-def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True):
+def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True, exact_edt=False):
+    """Run the CUDA path.  With debug=True the intermediate frames and D2 are requested (this
+    selects the exact-EDT kernel) and the surface-only call (default streaming kernel) is run
+    as well: the two surfaces must be bit-identical."""
     torch = _torch()
     dev = torch.device("cuda", 0)
     B = len(off) - 1
@@ -48,11 +51,19 @@ def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True):
             outs[k] = torch.full((B, H, nw), -1, dtype=torch.int32, device=dev)
         outs["D2"] = torch.full((B, H, W), 7, dtype=torch.int32, device=dev)
     S = torch.full((B, H, W), -5.0, dtype=torch.float32, device=dev)
-    with ieds().Builder(W, H, n_d, n_f, alpha=alpha, chunk_windows=chunk, device=0) as bld:
-        bld.build_batch(txy, toff, S, edge_bits=outs.get("E"), denoised_bits=outs.get("E_d"),
-                        filtered_bits=outs.get("E_df"), sqdist=outs.get("D2"))
+    S2 = torch.full((B, H, W), -5.0, dtype=torch.float32, device=dev)
+    with ieds().Builder(W, H, n_d, n_f, alpha=alpha, chunk_windows=chunk, device=0, exact_edt=exact_edt) as bld:
+        bld.build_batch(txy, toff, S2)
+        if debug:
+            bld.build_batch(txy, toff, S, edge_bits=outs.get("E"), denoised_bits=outs.get("E_d"),
+                            filtered_bits=outs.get("E_df"), sqdist=outs.get("D2"))
         bld.sync()
-    res = {"S": S.cpu().numpy()}
+    res = {"S": (S if debug else S2).cpu().numpy()}
+    if debug:
+        S2 = S2.cpu().numpy()
+        bad = S2 != res["S"]
+        assert not bad.any(), ("surface-only path differs from the exact path", int(bad.sum()),
+                               np.argwhere(bad)[:5])
     for k, v in outs.items():
         res[k] = v.cpu().numpy().view(np.uint32)
     return res
@@ -256,3 +267,37 @@ def test_full_size_bench_config_sampled():
         err = np.abs(Sh[i].astype(np.float64) - refs[i]["S"]).max()
         assert err <= TOL, (b, err)
         assert np.all((Sh[i] == 0) == (refs[i]["E_df"] == 1))
+
+
+# ----------------------------------------------------------------------------- streaming vs exact
+
+def _stress_windows(W, H, seed):
+    rng = np.random.default_rng(seed)
+    wins = []
+    yy, xx = np.mgrid[0:H, 0:W]
+    masks = [
+        (yy % 23 == 0), (xx % 29 == 0), ((xx + yy) % 37 == 0), ((xx - 2 * yy) % 41 == 0),
+        (yy == H // 2) & (xx % 3 == 0), ((xx // 7 + yy // 5) % 2 == 0) & (rng.random((H, W)) < 0.05),
+        rng.random((H, W)) < 0.0005, rng.random((H, W)) < 0.003, rng.random((H, W)) < 0.02,
+        (np.hypot(xx - W / 2, yy - H / 2).astype(int) % 31 == 0),
+    ]
+    for m in masks:
+        ys, xs = np.nonzero(m)
+        wins.append(pack_xy(xs, ys))
+    return wins
+
+
+@pytest.mark.parametrize("d_sat", [1.0, 3.0, 6.0, 8.0, 9.5])
+def test_streaming_surface_bit_identical_to_exact(d_sat):
+    """The saturation-aware streaming kernel (default when D2 is not requested) must produce the
+    same fp32 surface bits as the exact-EDT kernel, for every saturation radius it serves."""
+    W, H = 300, 211
+    wins = _stress_windows(W, H, int(d_sat * 10))
+    xy, off = csr(wins)
+    a = oracle.alpha_from_dsat(d_sat)
+    g_stream = run_gpu(xy, off, W, H, 0, 5, a, debug=False)
+    g_exact = run_gpu(xy, off, W, H, 0, 5, a, debug=False, exact_edt=True)
+    assert np.array_equal(g_stream["S"], g_exact["S"])
+    for b in (0, 6, 9):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, 0, 5, a)
+        assert np.abs(g_stream["S"][b] - ref["S"]).max() <= TOL
