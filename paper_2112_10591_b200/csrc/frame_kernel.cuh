@@ -29,7 +29,8 @@ struct FrameParams {
     uint32_t* __restrict__ E_out;           // [nb][H][NW] or null
     uint32_t* __restrict__ Ed_out;
     uint32_t* __restrict__ Edf_out;
-    uint32_t* __restrict__ Edf_scratch;     // [nb][H][NW] E_df for the streaming surface kernel
+    uint32_t* __restrict__ Edf_scratch;     // [nb][H][NW+2] E_df for the streaming surface kernel,
+                                            // word w at 1 + w, zero guard words at 0 and NW + 1
     int* __restrict__ err;
 };
 
@@ -171,7 +172,12 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
             const size_t o = ((size_t)b * p.H + y) * p.NW + w;
             if (p.Ed_out) p.Ed_out[o] = cd;
             if (p.Edf_out) p.Edf_out[o] = df;
-            if (p.Edf_scratch) p.Edf_scratch[o] = df;
+            if (p.Edf_scratch) {
+                uint32_t* row = p.Edf_scratch + ((size_t)b * p.H + y) * (p.NW + 2);
+                row[1 + w] = df;
+                if (w == 0) row[0] = 0u;
+                if (w == p.NW - 1) row[p.NW + 1] = 0u;
+            }
         }
         if (!p.T) continue;   // streaming surface kernel reads row-major E_df instead
         const uint32_t t = warp_transpose32(df, lane);

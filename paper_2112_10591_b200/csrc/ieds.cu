@@ -17,6 +17,7 @@
 #include "frame_kernel.cuh"
 #include "edt_kernel.cuh"
 #include "surface_kernel.cuh"
+#include "window_kernel.cuh"
 
 #ifndef IEDS_VERSION_STR
 #define IEDS_VERSION_STR "ieds-b200 0.1 (sm_100a)"
@@ -56,7 +57,8 @@ struct ieds_handle {
     int chunk;
     size_t smem_frame, smem_edt, smem_edt_d2;
     int c_sat;                 // ceil(sqrt(K_sat)): rows/columns a near site can be away
-    bool streaming;            // saturation-aware streaming surface kernel usable (c_sat <= 31)
+    int c_win;                 // window size of the branch-free kernel (>= c_sat)
+    bool streaming;            // saturation-aware window kernel usable (K_sat <= 1024)
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W]; streaming path: [chunk][H][NW] E_df
     unsigned long long* colmask = nullptr;
     int* err = nullptr;
@@ -140,6 +142,37 @@ void prof_pair(ieds_handle* h, int kind, cudaEvent_t* a, cudaEvent_t* b) {
     ++p.used;
 }
 
+// window sizes the branch-free kernel is instantiated for (c is rounded up: any C >= c is exact)
+constexpr int kWinSizes[] = {4, 6, 8, 10, 12, 14, 16, 19, 22, 25, 28, 32};
+
+int window_size_for(int c) {
+    for (int v : kWinSizes)
+        if (v >= c) return v;
+    return 0;
+}
+
+template <int C>
+void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp) {
+    ieds::window_kernel<C><<<grid, ieds::kWinWarps * 32, 0, st>>>(wp);
+}
+
+void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp) {
+    switch (C) {
+        case 4: launch_window_t<4>(grid, st, wp); break;
+        case 6: launch_window_t<6>(grid, st, wp); break;
+        case 8: launch_window_t<8>(grid, st, wp); break;
+        case 10: launch_window_t<10>(grid, st, wp); break;
+        case 12: launch_window_t<12>(grid, st, wp); break;
+        case 14: launch_window_t<14>(grid, st, wp); break;
+        case 16: launch_window_t<16>(grid, st, wp); break;
+        case 19: launch_window_t<19>(grid, st, wp); break;
+        case 22: launch_window_t<22>(grid, st, wp); break;
+        case 25: launch_window_t<25>(grid, st, wp); break;
+        case 28: launch_window_t<28>(grid, st, wp); break;
+        default: launch_window_t<32>(grid, st, wp); break;
+    }
+}
+
 int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int64_t n_events, int nb,
                  float* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st) {
     ieds::FrameParams fp;
@@ -174,21 +207,18 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     if (pb) cudaEventRecord(pb, st);
 
     if (stream_path) {
-        ieds::SurfParams sp;
-        sp.Edf = h->T;
-        sp.S = S;
-        sp.lut = h->lut;
-        sp.W = h->cfg.width;
-        sp.H = h->cfg.height;
-        sp.NW = h->NW;
-        sp.K_lut = h->K_lut;
-        sp.K_sat = h->K_sat;
-        sp.c = h->c_sat;
-        sp.c_exp = h->c_exp;
-        dim3 sgrid((h->NW + ieds::kSurfWarps - 1) / ieds::kSurfWarps, nb);
+        ieds::WinParams wp;
+        wp.Edf = h->T;
+        wp.S = S;
+        wp.lut = h->lut;
+        wp.W = h->cfg.width;
+        wp.H = h->cfg.height;
+        wp.NW = h->NW;
+        wp.K_sat = h->K_sat;
+        dim3 wgrid((h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps, nb);
         prof_pair(h, 1, &pa, &pb);
         if (pa) cudaEventRecord(pa, st);
-        ieds::surface_kernel<<<sgrid, ieds::kSurfWarps * 32, 0, st>>>(sp);
+        launch_window(h->c_win, wgrid, st, wp);
         if (pb) cudaEventRecord(pb, st);
         cudaError_t e2 = cudaGetLastError();
         return e2 == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
@@ -286,8 +316,8 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
         while (cs > 1 && (cs - 1) * (cs - 1) >= ksat) --cs;
         h->c_sat = (int)std::min<int64_t>(cs, 1 << 20);
     }
-    h->streaming = h->c_sat <= 31 && h->K_lut >= h->K_sat && H <= 2047 &&
-                   !(cfg->flags & IEDS_FLAG_EXACT_EDT);
+    h->c_win = window_size_for(std::max(2, h->c_sat));
+    h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT);
 
     h->smem_frame = 4ull * ((h->NWP * H + 3) & ~3) + 8ull * W;
     h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
@@ -307,15 +337,17 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
     if (e == cudaSuccess)
         e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk *
-                                  std::max<size_t>((size_t)h->NR * W, (size_t)h->NW * H));
+                                  std::max<size_t>((size_t)h->NR * W, (size_t)(h->NW + 2) * H));
     if (e == cudaSuccess) e = cudaMalloc(&h->colmask, sizeof(unsigned long long) * (size_t)h->chunk * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMallocHost(&h->h_err, sizeof(int));
-    if (e == cudaSuccess) e = cudaMalloc(&h->lut, sizeof(float) * std::max(1, h->K_lut));
+    // table of Eq. (1) over integer D2 < K_lut, plus one saturated entry (1.0f) at K_lut
+    if (e == cudaSuccess) e = cudaMalloc(&h->lut, sizeof(float) * (h->K_lut + 1));
     if (e == cudaSuccess) {
-        std::vector<float> lut(std::max(1, h->K_lut));
+        std::vector<float> lut(h->K_lut + 1);
         for (int i = 0; i < h->K_lut; ++i) lut[i] = surface_f32((double)i, alpha);
+        lut[h->K_lut] = 1.0f;
         e = cudaMemcpy(h->lut, lut.data(), sizeof(float) * lut.size(), cudaMemcpyHostToDevice);
     }
     if (e != cudaSuccess) {
