@@ -48,7 +48,7 @@ __device__ __forceinline__ constexpr uint32_t slot_sq(int slot, int u_phase) {
 }
 
 template <int C>
-__global__ void __launch_bounds__(kWinWarps * 32) window_kernel(WinParams p) {
+__global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 6 : 3)) window_kernel(WinParams p) {
     static_assert(C >= 2 && C <= 64, "window size");
     constexpr int NS = 2 * C;   // slots
     __shared__ float lut_s[1025];
@@ -64,26 +64,51 @@ __global__ void __launch_bounds__(kWinWarps * 32) window_kernel(WinParams p) {
     const int NWP2 = p.NW + 2;
     const int x = 32 * w + lane;
     const bool xvalid = x < W;
-    const uint32_t* rp = p.Edf + (size_t)b * H * NWP2 + 1 + w;
-    float* sp = p.S + (size_t)b * H * W + (xvalid ? x : 0);
+    const uint32_t* rp = p.Edf + (size_t)b * H * NWP2 + w;   // words w-1, w, w+1 at rp[0..2]
+    float* op = p.S + (size_t)b * H * W + (xvalid ? x : 0);  // next pixel to emit (rows in order)
+    const size_t wstride = (size_t)W;
 
     uint32_t R[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) R[k] = 0xFFFFFFFFu;
 
-    const uint32_t* q = rp;   // row u0
-    float* op = sp;           // next pixel to emit (rows are emitted in order)
+    // The strip's three words of 32 consecutive rows are fetched lane-parallel (lane i holds
+    // row base+i) one batch ahead and broadcast with shuffles when the row is processed.
+    uint32_t cl = 0, cm = 0, cr = 0, nl = 0, nm = 0, nr = 0;
+    auto fetch = [&](int row0, uint32_t& a, uint32_t& m, uint32_t& z) {
+        const int r = row0 + lane;
+        if (r < H) {
+            const uint32_t* q = rp + (size_t)r * NWP2;
+            a = __ldg(q);
+            m = __ldg(q + 1);
+            z = __ldg(q + 2);
+        } else {
+            a = m = z = 0u;
+        }
+    };
+    fetch(0, cl, cm, cr);
+    fetch(32, nl, nm, nr);
+    auto h_of = [&](int u) -> uint32_t {   // h of row u clamped to C (rows >= H: no site)
+        const int src = u & 31;
+        const uint32_t tl = __shfl_sync(0xFFFFFFFFu, cl, src);
+        const uint32_t t = __shfl_sync(0xFFFFFFFFu, cm, src);
+        const uint32_t tr = __shfl_sync(0xFFFFFFFFu, cr, src);
+        return (uint32_t)min(hdist_words(tl, t, tr, lane), C);
+    };
+
     const int total = H + C - 1;   // rows u = 0 .. total-1: push site u (< H), emit u-C+1 (>= 0)
     for (int base = 0; base < total; base += NS) {
 #pragma unroll
         for (int ph = 0; ph < NS; ph += 2) {
             const int u0 = base + ph;
             if (u0 >= total) break;
-            // h of rows u0, u0+1 clamped to C (rows >= H have no site)
-            uint32_t ha = (uint32_t)C, hb = (uint32_t)C;
-            if (u0 < H) ha = (uint32_t)min(hdist_words(q[-1], q[0], q[1], lane), C);
-            if (u0 + 1 < H) hb = (uint32_t)min(hdist_words(q[NWP2 - 1], q[NWP2], q[NWP2 + 1], lane), C);
-            q += 2 * NWP2;
+            if (u0 > 0 && (u0 & 31) == 0) {   // rows u0.. start a new batch of 32
+                cl = nl;
+                cm = nm;
+                cr = nr;
+                fetch(u0 + 32, nl, nm, nr);
+            }
+            const uint32_t ha = h_of(u0), hb = h_of(u0 + 1);   // rows >= H read zero words
             // skip the update when no lane of either row has a site within C-1 columns
             if (__any_sync(0xFFFFFFFFu, (ha < (uint32_t)C) | (hb < (uint32_t)C))) {
                 const uint32_t h2a = ha * ha * 0x10001u, h2b = hb * hb * 0x10001u;
@@ -104,8 +129,11 @@ __global__ void __launch_bounds__(kWinWarps * 32) window_kernel(WinParams p) {
                 if (yo >= 0 && yo < H) {
                     const uint32_t v = (so & 1) ? (R[so >> 1] >> 16) : (R[so >> 1] & 0xFFFFu);
                     const float f = lut_s[min(v, K_sat)];
-                    if (xvalid) *op = f;
-                    op += W;
+                    // write-once output: streaming store, predicated off for lanes beyond W
+                    asm volatile(
+                        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
+                        ::"l"(op), "f"(f), "r"((uint32_t)xvalid) : "memory");
+                    op += wstride;
                 }
                 R[so >> 1] |= (so & 1) ? 0xFFFF0000u : 0x0000FFFFu;
             }
