@@ -6,9 +6,11 @@
 //   then         E_df is transposed into column words T (bit i of T[r][x] = E_df(x, 32r+i))
 //                plus a per-column bitmap of non-empty word-rows, which is all the EDT needs.
 //
-// Layout: the frame lives in shared memory as H rows of NWP = (ceil(W/32) | 1) words (an odd
-// row stride makes the "lane = row" accesses below bank-conflict free).  Bit (x % 32) of word
-// x / 32 is pixel x; bits beyond W stay 0.  Out-of-frame neighbours count as non-edge.
+// Layout: the frame lives in shared memory as H + 2 rows of NWP words, NWP = the smallest odd
+// number > ceil(W/32) (an odd row stride makes the "lane = row" accesses bank-conflict free and
+// leaves at least one zero pad word per row).  Frame row y is shared row y + 1; rows 0 and H+1
+// and the pad words are zero, so out-of-frame neighbours read as non-edge (reading R1) without
+// bounds checks.  Bit (x % 32) of word x / 32 is pixel x; bits beyond W stay 0.
 #pragma once
 #include <cstdint>
 
@@ -47,7 +49,7 @@ __device__ __forceinline__ uint32_t at_least(int n, uint32_t a, uint32_t b, uint
 }
 
 __device__ __forceinline__ uint32_t frame_word(const uint32_t* fr, const FrameParams& p, int y, int w) {
-    return (y >= 0 && y < p.H && w >= 0 && w < p.NW) ? fr[y * p.NWP + w] : 0u;
+    return (y >= 0 && y < p.H && w >= 0 && w < p.NW) ? fr[(y + 1) * p.NWP + w] : 0u;
 }
 
 // E_d word (y, w): Alg. 1 on 32 pixels at once.
@@ -64,7 +66,7 @@ __device__ __forceinline__ uint32_t denoised_word(const uint32_t* fr, const Fram
 __device__ __forceinline__ uint32_t scatter_event(uint32_t* fr, const FrameParams& p, uint32_t v) {
     uint32_t x = v & 0xFFFFu, y = v >> 16;
     if (x < (uint32_t)p.W && y < (uint32_t)p.H) {
-        atomicOr(&fr[y * p.NWP + (x >> 5)], 1u << (x & 31));
+        atomicOr(&fr[(y + 1) * p.NWP + (x >> 5)], 1u << (x & 31));
         return 0u;
     }
     return 1u;
@@ -93,9 +95,106 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, int lane) {
     return v;
 }
 
+// E_d / E_df of one frame word from its shared-memory neighbourhood (guard rows/pad words = 0)
+template <int N>
+__device__ __forceinline__ uint32_t stencil_word(const uint32_t* fr, int i, int NWP) {
+    const uint32_t c = fr[i];
+    const uint32_t lf = (c << 1) | (fr[i - 1] >> 31);
+    const uint32_t rt = (c >> 1) | (fr[i + 1] << 31);
+    return at_least(N, fr[i - NWP], fr[i + NWP], lf, rt);
+}
+
+constexpr int kDfWords = 16;   // frame words staged per thread per round of the in-place pass
+
+// Alg. 1 in place (E -> E_d) in rounds of row bands whose E_d words are staged in registers
+// between barriers; the last E row of a band is saved before it is overwritten, because the
+// next band's first row needs it as its upper neighbour.  Then Alg. 2 reads E_d and writes
+// the row-major E_df scratch (word w of row y at [y][1 + w]; the guard words stay 0).
+// sv: 2 * NWP words of shared scratch for the saved rows.
+template <int ND, int NF>
+__device__ __forceinline__ void denoise_fill_inplace(uint32_t* fr, uint32_t* sv, const FrameParams& p, int b,
+                                                     int tid, int nthr) {
+    const int NWP = p.NWP, H = p.H;
+    const int rows_per_round = max(1, (kDfWords * nthr) / NWP);
+    uint32_t* prevE = sv;          // E of the row above the current band (zeros for band 0)
+    uint32_t* saveE = sv + NWP;
+    for (int i = tid; i < NWP; i += nthr) prevE[i] = 0u;
+    __syncthreads();
+    for (int r0 = 0; r0 < H; r0 += rows_per_round) {
+        const int r1 = min(H, r0 + rows_per_round);
+        const int lo = (r0 + 1) * NWP, hi = (r1 + 1) * NWP;
+        uint32_t ed[kDfWords];
+#pragma unroll
+        for (int k = 0; k < kDfWords; ++k) {
+            const int i = lo + tid + k * nthr;
+            uint32_t v = 0u;
+            if (i < hi) {
+                const uint32_t c = fr[i];
+                const uint32_t up = (i < lo + NWP) ? prevE[i - lo] : fr[i - NWP];
+                const uint32_t lf = (c << 1) | (fr[i - 1] >> 31);
+                const uint32_t rt = (c >> 1) | (fr[i + 1] << 31);
+                v = c & at_least(ND, up, fr[i + NWP], lf, rt);
+            }
+            ed[k] = v;
+        }
+        for (int i = tid; i < NWP; i += nthr) saveE[i] = fr[(r1 - 1 + 1) * NWP + i];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kDfWords; ++k) {
+            const int i = lo + tid + k * nthr;
+            if (i < hi) fr[i] = ed[k];
+        }
+        uint32_t* t = prevE;
+        prevE = saveE;
+        saveE = t;
+        __syncthreads();
+    }
+    const uint32_t lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : kFull;
+    const size_t NW2 = (size_t)p.NW + 2;
+    uint32_t* scratch = p.Edf_scratch + (size_t)b * H * NW2;
+    const int n = H * NWP;
+    for (int j = tid; j < n; j += nthr) {
+        const int y = j / NWP, w = j - y * NWP;
+        if (w >= p.NW) continue;
+        const int i = j + NWP;
+        const uint32_t c = fr[i];
+        const uint32_t lf = (c << 1) | (fr[i - 1] >> 31);
+        const uint32_t rt = (c >> 1) | (fr[i + 1] << 31);
+        uint32_t df = c | at_least(NF, fr[i - NWP], fr[i + NWP], lf, rt);
+        if (w == p.NW - 1) df &= lastmask;
+        scratch[(size_t)y * NW2 + 1 + w] = df;
+        const size_t o = ((size_t)b * H + y) * p.NW + w;
+        if (p.Ed_out) p.Ed_out[o] = c;
+        if (p.Edf_out) p.Edf_out[o] = df;
+    }
+}
+
+template <int ND>
+__device__ __forceinline__ void denoise_fill_nf(uint32_t* fr, uint32_t* sv, const FrameParams& p, int b, int tid,
+                                                int nthr) {
+    switch (p.n_f) {
+        case 1: denoise_fill_inplace<ND, 1>(fr, sv, p, b, tid, nthr); break;
+        case 2: denoise_fill_inplace<ND, 2>(fr, sv, p, b, tid, nthr); break;
+        case 3: denoise_fill_inplace<ND, 3>(fr, sv, p, b, tid, nthr); break;
+        case 4: denoise_fill_inplace<ND, 4>(fr, sv, p, b, tid, nthr); break;
+        default: denoise_fill_inplace<ND, 5>(fr, sv, p, b, tid, nthr); break;
+    }
+}
+
+__device__ __forceinline__ void streaming_denoise_fill(uint32_t* fr, uint32_t* sv, const FrameParams& p, int b,
+                                                       int tid, int nthr) {
+    switch (p.n_d) {
+        case 0: denoise_fill_nf<0>(fr, sv, p, b, tid, nthr); break;
+        case 1: denoise_fill_nf<1>(fr, sv, p, b, tid, nthr); break;
+        case 2: denoise_fill_nf<2>(fr, sv, p, b, tid, nthr); break;
+        case 3: denoise_fill_nf<3>(fr, sv, p, b, tid, nthr); break;
+        default: denoise_fill_nf<4>(fr, sv, p, b, tid, nthr); break;
+    }
+}
+
 __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    const int nframe = p.H * p.NWP;
+    const int nframe = (p.H + 2) * p.NWP;
     uint32_t* fr = smem;
     unsigned long long* cm = reinterpret_cast<unsigned long long*>(smem + ((nframe + 3) & ~3));
     const int b = blockIdx.x;
@@ -147,7 +246,12 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
 
     if (p.E_out) {
         uint32_t* out = p.E_out + (size_t)b * p.H * p.NW;
-        for (int i = tid; i < p.H * p.NW; i += nthr) out[i] = fr[(i / p.NW) * p.NWP + (i % p.NW)];
+        for (int i = tid; i < p.H * p.NW; i += nthr) out[i] = fr[(i / p.NW + 1) * p.NWP + (i % p.NW)];
+    }
+
+    if (!p.T) {   // streaming surface path: row-major E_df only
+        streaming_denoise_fill(fr, reinterpret_cast<uint32_t*>(cm), p, b, tid, nthr);
+        return;
     }
 
     // ---- a2 + a3 on 32x32 blocks (lane = row), then transpose the block into T
@@ -172,14 +276,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
             const size_t o = ((size_t)b * p.H + y) * p.NW + w;
             if (p.Ed_out) p.Ed_out[o] = cd;
             if (p.Edf_out) p.Edf_out[o] = df;
-            if (p.Edf_scratch) {
-                uint32_t* row = p.Edf_scratch + ((size_t)b * p.H + y) * (p.NW + 2);
-                row[1 + w] = df;
-                if (w == 0) row[0] = 0u;
-                if (w == p.NW - 1) row[p.NW + 1] = 0u;
-            }
         }
-        if (!p.T) continue;   // streaming surface kernel reads row-major E_df instead
         const uint32_t t = warp_transpose32(df, lane);
         const int x = 32 * w + lane;
         if (x < p.W) {
@@ -187,7 +284,6 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
             if (t) atomicOr(&cm[x], 1ull << r);
         }
     }
-    if (!p.T) return;
     __syncthreads();
     for (int x = tid; x < p.W; x += nthr) p.colmask[(size_t)b * p.W + x] = cm[x];
 }

@@ -59,7 +59,8 @@ struct ieds_handle {
     int c_sat;                 // ceil(sqrt(K_sat)): rows/columns a near site can be away
     int c_win;                 // window size of the branch-free kernel (>= c_sat)
     bool streaming;            // saturation-aware window kernel usable (K_sat <= 1024)
-    uint32_t* T = nullptr;     // exact path: [chunk][NR][W]; streaming path: [chunk][H][NW] E_df
+    uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
+    uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
     unsigned long long* colmask = nullptr;
     int* err = nullptr;
     int* h_err = nullptr;   // pinned
@@ -198,7 +199,7 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     if (stream_path) {
         fp.T = nullptr;
         fp.colmask = nullptr;
-        fp.Edf_scratch = h->T;
+        fp.Edf_scratch = h->Edfs;
     }
     cudaEvent_t pa, pb;
     prof_pair(h, 0, &pa, &pb);
@@ -208,7 +209,7 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
 
     if (stream_path) {
         ieds::WinParams wp;
-        wp.Edf = h->T;
+        wp.Edf = h->Edfs;
         wp.S = S;
         wp.lut = h->lut;
         wp.W = h->cfg.width;
@@ -295,7 +296,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
         return IEDS_ECUDA;
     }
     h->NW = (W + 31) / 32;
-    h->NWP = h->NW | 1;
+    h->NWP = (h->NW + 1) | 1;   // odd, with >= 1 zero pad word per row
     h->NR = (H + 31) / 32;
     int ns = (W + kSegTarget - 1) / kSegTarget;
     ns = std::max(1, std::min(16, ns));
@@ -319,10 +320,12 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->c_win = window_size_for(std::max(2, h->c_sat));
     h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT);
 
-    h->smem_frame = 4ull * ((h->NWP * H + 3) & ~3) + 8ull * W;
+    // frame + (column bitmap for the exact path | two saved rows for the streaming path)
+    h->smem_frame = 4ull * (((H + 2) * h->NWP + 3) & ~3) + 8ull * std::max(W, h->NWP);
     h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
     h->smem_edt_d2 = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, true);
-    if (h->smem_frame > (size_t)kMaxSmem || h->smem_edt_d2 > (size_t)kMaxSmem || h->SEGW > 255) {
+    if (h->smem_frame > (size_t)kMaxSmem || h->smem_edt_d2 > (size_t)kMaxSmem || h->SEGW > 255 ||
+        h->NWP > ieds::kDfWords * kFrameThreads) {
         delete h;
         return IEDS_EINVAL;
     }
@@ -335,9 +338,9 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
-    if (e == cudaSuccess)
-        e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk *
-                                  std::max<size_t>((size_t)h->NR * W, (size_t)(h->NW + 2) * H));
+    if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
+    if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
+    if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMalloc(&h->colmask, sizeof(unsigned long long) * (size_t)h->chunk * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(int));
@@ -367,6 +370,7 @@ void ieds_destroy(ieds_handle* h) {
     free_host_path(h->hp);
     for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
     cudaFree(h->T);
+    cudaFree(h->Edfs);
     cudaFree(h->colmask);
     cudaFree(h->err);
     cudaFree(h->lut);
