@@ -30,8 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from synth.events import WORKLOADS, batch_events  # noqa: E402
+from paper_2112_10591_b200.multi import shard  # noqa: E402
 
-EDT_KERNEL_NAME = "surface_kernel (a4 EDT, saturation-aware streaming + a5 surface)"
+EDT_KERNEL_NAME = "window_kernel<C> (a4 EDT, saturation-aware register window + a5 surface)"
 METRIC = "IEDS surfaces/sec and Mev/s at 1280x720 (1/2/4/8 B200), % HBM peak"
 UNIT = "surfaces/s"
 
@@ -43,6 +44,24 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_per_launch(override, windows_per_launch):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/*_traffic.json, scaled to this run's windows per launch), or None."""
+    if override is not None:
+        return override
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as f:
+            t = json.load(f)
+        return t["dram_bytes_per_launch"] / t["windows_per_launch"] * windows_per_launch
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------------------------- inputs
@@ -232,7 +251,7 @@ def run_ours(args):
     c = wl.scene
     W, H = c.width, c.height
     nwin = args.windows or wl.n_windows
-    k0 = rank * nwin
+    k0 = shard(nwin * world, world, rank).start   # weak scaling: nwin distinct windows per rank
     xy, off = generate(args.config, k0, nwin)
     n_ev = len(xy)
     txy = torch.from_numpy(xy.view(np.int32)).to(dev)
@@ -358,7 +377,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
-        n_s = cores * max(1, args.cpu_windows_per_core)
+        n_s = max(cores, args.cpu_windows)
         r, done, wall = oracle_rate(args.config, n_s, cores)
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{done} windows of {wl.name} (distinct seeds), {cores} processes, "
@@ -380,13 +399,15 @@ def run_ours(args):
                           "note": "algorithmic bytes of the whole path: 4 B/event + 4 B/px + offsets"},
         "roofline": {"bound": "hbm", "kernel": EDT_KERNEL_NAME,
                      "achieved": edt_gbs, "peak": peak, "unit": "GB/s", "frac": edt_gbs / peak,
-                     "traffic": args.traffic, "peak_source": peak_src,
+                     "traffic": traffic_per_launch(args.traffic, nwin / max(1, edt_n // args.steps)),
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": edt_bytes_per_launch, "avg_launch_ms": edt_avg_ms,
                      "share_of_step": edt_ms / max(1e-9, ms_max)},
         "kernels": {"frame_kernel": {"avg_ms": fr_avg_ms, "launches": fr_n,
                                      "achieved_gbs": fr_bytes_per_launch / (fr_avg_ms / 1e3) / 1e9 if fr_avg_ms else None,
                                      "share_of_step": fr_ms / max(1e-9, ms_max)},
-                    "edt_kernel": {"avg_ms": edt_avg_ms, "launches": edt_n}},
+                    "window_kernel": {"avg_ms": edt_avg_ms, "launches": edt_n,
+                                      "share_of_step": edt_ms / max(1e-9, ms_max)}},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clocks,
         "e2e": e2e,
@@ -410,7 +431,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-EDT comparison run")
-    ap.add_argument("--cpu-windows-per-core", type=int, default=4)
+    ap.add_argument("--cpu-windows", type=int, default=256,
+                    help="oracle windows timed for cpu_baseline (~15 core-seconds at 1280x720)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per EDT launch (from profiles/), reported in roofline.traffic")
     args = ap.parse_args()
