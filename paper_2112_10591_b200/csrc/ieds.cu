@@ -16,7 +16,6 @@
 #include "../../include/ieds.h"
 #include "frame_kernel.cuh"
 #include "edt_kernel.cuh"
-#include "surface_kernel.cuh"
 #include "window_kernel.cuh"
 
 #ifndef IEDS_VERSION_STR

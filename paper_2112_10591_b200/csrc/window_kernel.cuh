@@ -39,43 +39,35 @@ __device__ __forceinline__ int hdist_words(uint32_t tl, uint32_t t, uint32_t tr,
     return min(__clz(left), __clz(__brev(right)));
 }
 
+// squared distance from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
 template <int C>
-__device__ __forceinline__ constexpr uint32_t slot_sq(int slot, int u_phase) {
-    // distance from row u (u == u_phase mod 2C) to the window pixel held in `slot`
-    // (window = [u-C+1, u+C]): d = ((slot - u_phase + C - 1) mod 2C) - (C - 1)
-    const int d = ((slot - u_phase + C - 1) % (2 * C) + 2 * C) % (2 * C) - (C - 1);
+__device__ __forceinline__ constexpr uint32_t dsq(int j, int row_off) {
+    const int d = j - (C - 1) - row_off;
     return (uint32_t)(d * d);
 }
 
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// write-once output: streaming store, predicated off for lanes beyond W
+__device__ __forceinline__ void st_cs_pred(float* ptr, float v, uint32_t pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
+                 ::"l"(ptr), "f"(v), "r"(pred) : "memory");
+}
+
 template <int C>
-__global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 6 : 3)) window_kernel(WinParams p) {
-    static_assert(C >= 2 && C <= 64, "window size");
-    constexpr int NS = 2 * C;   // slots
-    __shared__ float lut_s[1025];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) lut_s[i] = p.lut[i];
-    __syncthreads();
+struct WinState {
+    const uint32_t* rp;   // this strip's words of row 0 (words w-1, w, w+1 at rp[0..2])
+    int H, NWP2, lane;
+    uint32_t cl, cm, cr, nl, nm, nr;   // current / next batch of 32 rows (lane i = row base+i)
+    float* op;                         // next pixel to emit
+    size_t W;
+    uint32_t lut_sh, K_sat, xvalid;
 
-    const int w = blockIdx.x * kWinWarps + warp;
-    if (w >= p.NW) return;
-    const int b = blockIdx.y;
-    const int W = p.W, H = p.H;
-    const uint32_t K_sat = (uint32_t)p.K_sat;
-    const int NWP2 = p.NW + 2;
-    const int x = 32 * w + lane;
-    const bool xvalid = x < W;
-    const uint32_t* rp = p.Edf + (size_t)b * H * NWP2 + w;   // words w-1, w, w+1 at rp[0..2]
-    float* op = p.S + (size_t)b * H * W + (xvalid ? x : 0);  // next pixel to emit (rows in order)
-    const size_t wstride = (size_t)W;
-
-    uint32_t R[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) R[k] = 0xFFFFFFFFu;
-
-    // The strip's three words of 32 consecutive rows are fetched lane-parallel (lane i holds
-    // row base+i) one batch ahead and broadcast with shuffles when the row is processed.
-    uint32_t cl = 0, cm = 0, cr = 0, nl = 0, nm = 0, nr = 0;
-    auto fetch = [&](int row0, uint32_t& a, uint32_t& m, uint32_t& z) {
+    __device__ __forceinline__ void fetch(int row0, uint32_t& a, uint32_t& m, uint32_t& z) const {
         const int r = row0 + lane;
         if (r < H) {
             const uint32_t* q = rp + (size_t)r * NWP2;
@@ -85,59 +77,86 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 6 : 3)) window_kern
         } else {
             a = m = z = 0u;
         }
-    };
-    fetch(0, cl, cm, cr);
-    fetch(32, nl, nm, nr);
-    auto h_of = [&](int u) -> uint32_t {   // h of row u clamped to C (rows >= H: no site)
-        const int src = u & 31;
+    }
+    __device__ __forceinline__ uint32_t h_of(int src) const {
         const uint32_t tl = __shfl_sync(0xFFFFFFFFu, cl, src);
         const uint32_t t = __shfl_sync(0xFFFFFFFFu, cm, src);
         const uint32_t tr = __shfl_sync(0xFFFFFFFFu, cr, src);
-        return (uint32_t)min(hdist_words(tl, t, tr, lane), C);
-    };
+        return (uint32_t)hdist_words(tl, t, tr, lane);   // <= 32; >= C contributes >= C^2
+    }
+    __device__ __forceinline__ void emit(uint32_t v) {
+        st_cs_pred(op, lds_f32(lut_sh + 4u * min(v, K_sat)), xvalid);
+        op += W;
+    }
 
-    const int total = H + C - 1;   // rows u = 0 .. total-1: push site u (< H), emit u-C+1 (>= 0)
-    for (int base = 0; base < total; base += NS) {
-#pragma unroll
-        for (int ph = 0; ph < NS; ph += 2) {
-            const int u0 = base + ph;
-            if (u0 >= total) break;
-            if (u0 > 0 && (u0 & 31) == 0) {   // rows u0.. start a new batch of 32
-                cl = nl;
-                cm = nm;
-                cr = nr;
-                fetch(u0 + 32, nl, nm, nr);
-            }
-            const uint32_t ha = h_of(u0), hb = h_of(u0 + 1);   // rows >= H read zero words
-            // skip the update when no lane of either row has a site within C-1 columns
-            if (__any_sync(0xFFFFFFFFu, (ha < (uint32_t)C) | (hb < (uint32_t)C))) {
-                const uint32_t h2a = ha * ha * 0x10001u, h2b = hb * hb * 0x10001u;
-#pragma unroll
-                for (int k = 0; k < C; ++k) {
-                    // rows u0 (phase ph) and u0+1 (phase ph+1); slots 2k (low half), 2k+1 (high)
-                    const uint32_t sqa = slot_sq<C>(2 * k, ph) | (slot_sq<C>(2 * k + 1, ph) << 16);
-                    const uint32_t sqb = slot_sq<C>(2 * k, ph + 1) | (slot_sq<C>(2 * k + 1, ph + 1) << 16);
-                    R[k] = __vminu2(R[k], __vminu2(sqa + h2a, sqb + h2b));
-                }
-            }
-            // pixels u0-C+1 and u0-C+2 are final: a row C or more away cannot bring a value
-            // below C^2 >= K_sat.  Their slots are reset for pixels u0+C+1, u0+C+2.
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int yo = u0 + e - (C - 1);
-                const int so = ((ph + e - (C - 1)) % NS + NS) % NS;   // compile-time slot of yo
-                if (yo >= 0 && yo < H) {
-                    const uint32_t v = (so & 1) ? (R[so >> 1] >> 16) : (R[so >> 1] & 0xFFFFu);
-                    const float f = lut_s[min(v, K_sat)];
-                    // write-once output: streaming store, predicated off for lanes beyond W
-                    asm volatile(
-                        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
-                        ::"l"(op), "f"(f), "r"((uint32_t)xvalid) : "memory");
-                    op += wstride;
-                }
-                R[so >> 1] |= (so & 1) ? 0xFFFF0000u : 0x0000FFFFu;
-            }
+    // Apply the sites of rows u, u+1 to the window and shift it by one register:
+    // dst[k] = min(src[k+1], parabolas of rows u, u+1 at pixels y0+2k, y0+2k+1), y0 = u-C+1.
+    // Afterwards pixels y0, y0+1 (dst[0]) are final -- a site C or more rows away cannot bring a
+    // value below C^2 >= K_sat -- and are emitted.
+    __device__ __forceinline__ void step(int u, const uint32_t (&src)[C], uint32_t (&dst)[C]) {
+        if (u > 0 && (u & 31) == 0) {   // rows u.. start a new batch of 32
+            cl = nl;
+            cm = nm;
+            cr = nr;
+            fetch(u + 32, nl, nm, nr);
         }
+        const uint32_t ha = h_of(u & 31), hb = h_of((u & 31) + 1);   // rows >= H: no site
+        if (__any_sync(0xFFFFFFFFu, (ha < (uint32_t)C) | (hb < (uint32_t)C))) {
+            const uint32_t h2a = ha * ha * 0x10001u, h2b = hb * hb * 0x10001u;
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const uint32_t sqa = dsq<C>(2 * k, 0) | (dsq<C>(2 * k + 1, 0) << 16);
+                const uint32_t sqb = dsq<C>(2 * k, 1) | (dsq<C>(2 * k + 1, 1) << 16);
+                const uint32_t prev = (k + 1 < C) ? src[k + 1 < C ? k + 1 : 0] : 0xFFFFFFFFu;
+                dst[k] = __vminu2(prev, __vminu2(sqa + h2a, sqb + h2b));
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < C; ++k) dst[k] = (k + 1 < C) ? src[k + 1 < C ? k + 1 : 0] : 0xFFFFFFFFu;
+        }
+        const int y0 = u - (C - 1);
+        if (y0 >= 0 && y0 < H) emit(dst[0] & 0xFFFFu);
+        if (y0 + 1 >= 0 && y0 + 1 < H) emit(dst[0] >> 16);
+    }
+};
+
+template <int C>
+__global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 4 : 3)) window_kernel(WinParams p) {
+    static_assert(C >= 2 && C <= 64, "window size");
+    __shared__ float lut_s[1025];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) lut_s[i] = p.lut[i];
+    __syncthreads();
+
+    const int w = blockIdx.x * kWinWarps + warp;
+    if (w >= p.NW) return;
+    const int b = blockIdx.y;
+    const int H = p.H;
+    const int x = 32 * w + lane;
+    WinState<C> st;
+    st.rp = p.Edf + (size_t)b * H * (p.NW + 2) + w;
+    st.H = H;
+    st.NWP2 = p.NW + 2;
+    st.lane = lane;
+    st.W = (size_t)p.W;
+    st.xvalid = x < p.W ? 1u : 0u;
+    st.op = p.S + (size_t)b * H * p.W + (x < p.W ? x : 0);
+    st.K_sat = (uint32_t)p.K_sat;
+    uint32_t lut_sh = (uint32_t)__cvta_generic_to_shared(lut_s);
+    asm volatile("" : "+r"(lut_sh));   // keep the shared address in a register
+    st.lut_sh = lut_sh;
+    st.fetch(0, st.cl, st.cm, st.cr);
+    st.fetch(32, st.nl, st.nm, st.nr);
+
+    // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
+    // Two register sets alternate (A -> B -> A) so the per-step shift needs no moves.
+    uint32_t A[C], B[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) A[k] = 0xFFFFFFFFu;
+    const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
+    for (int u = 0; u < total; u += 4) {
+        st.step(u, A, B);
+        if (u + 2 < total) st.step(u + 2, B, A);
     }
 }
 
