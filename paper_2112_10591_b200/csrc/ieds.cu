@@ -143,7 +143,7 @@ void prof_pair(ieds_handle* h, int kind, cudaEvent_t* a, cudaEvent_t* b) {
 }
 
 // window sizes the branch-free kernel is instantiated for (c is rounded up: any C >= c is exact)
-constexpr int kWinSizes[] = {4, 6, 8, 10, 12, 14, 16, 19, 22, 25, 28, 32};
+constexpr int kWinSizes[] = {4, 6, 8, 10, 12, 14, 16, 19, 22, 25, 28, 31};
 
 int window_size_for(int c) {
     for (int v : kWinSizes)
@@ -169,7 +169,7 @@ void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp)
         case 22: launch_window_t<22>(grid, st, wp); break;
         case 25: launch_window_t<25>(grid, st, wp); break;
         case 28: launch_window_t<28>(grid, st, wp); break;
-        default: launch_window_t<32>(grid, st, wp); break;
+        default: launch_window_t<31>(grid, st, wp); break;
     }
 }
 

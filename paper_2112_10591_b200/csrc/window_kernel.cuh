@@ -36,7 +36,8 @@ struct WinParams {
 __device__ __forceinline__ int hdist_words(uint32_t tl, uint32_t t, uint32_t tr, int j) {
     const uint32_t left = __funnelshift_rc(tl, t, j + 1);   // columns x-31..x, x in the MSB
     const uint32_t right = __funnelshift_r(t, tr, j);       // columns x..x+31, x in the LSB
-    return min(__clz(left), __clz(__brev(right)));
+    // trailing zeros of `right`; an empty word reads as 31, which is >= C for every C <= 31
+    return min(__clz(left), __ffs(right | 0x80000000u) - 1);
 }
 
 // squared distance from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
@@ -63,8 +64,8 @@ struct WinState {
     const uint32_t* rp;   // this strip's words of row 0 (words w-1, w, w+1 at rp[0..2])
     int H, NWP2, lane;
     uint32_t cl, cm, cr, nl, nm, nr;   // current / next batch of 32 rows (lane i = row base+i)
-    float* op;                         // next pixel to emit
-    size_t W;
+    float* op;                         // next pixel to emit (rows are emitted in order)
+    size_t W;                          // row stride in elements
     uint32_t lut_sh, K_sat, xvalid;
 
     __device__ __forceinline__ void fetch(int row0, uint32_t& a, uint32_t& m, uint32_t& z) const {
@@ -78,22 +79,29 @@ struct WinState {
             a = m = z = 0u;
         }
     }
-    __device__ __forceinline__ uint32_t h_of(int src) const {
+    __device__ __forceinline__ uint32_t h_of(int src_u) const {
+        int src = src_u;
+        asm volatile("mov.b32 %0, %0;" : "+r"(src));   // one vector copy of the lane index
         const uint32_t tl = __shfl_sync(0xFFFFFFFFu, cl, src);
         const uint32_t t = __shfl_sync(0xFFFFFFFFu, cm, src);
         const uint32_t tr = __shfl_sync(0xFFFFFFFFu, cr, src);
         return (uint32_t)hdist_words(tl, t, tr, lane);   // <= 32; >= C contributes >= C^2
     }
     __device__ __forceinline__ void emit(uint32_t v) {
-        st_cs_pred(op, lds_f32(lut_sh + 4u * min(v, K_sat)), xvalid);
+        const float f = lds_f32(lut_sh + 4u * min(v, K_sat));
+        if (xvalid) __stcs(op, f);   // write-once output: streaming (evict-first) store
         op += W;
     }
 
-    // Apply the sites of rows u, u+1 to the window and shift it by one register:
-    // dst[k] = min(src[k+1], parabolas of rows u, u+1 at pixels y0+2k, y0+2k+1), y0 = u-C+1.
-    // Afterwards pixels y0, y0+1 (dst[0]) are final -- a site C or more rows away cannot bring a
-    // value below C^2 >= K_sat -- and are emitted.
-    __device__ __forceinline__ void step(int u, const uint32_t (&src)[C], uint32_t (&dst)[C]) {
+    // Rotating window: before a pair step of phase S, logical register j (pixels y0+2j,
+    // y0+2j+1 with y0 = u-C+1) lives in P[(j + S) % C].  The step applies the sites of rows
+    // u, u+1 and shifts the window by one register, in place: logical j of the new window is
+    // old logical j+1 min the two parabolas, and the freed register P[S % C] becomes the new
+    // last register.  Then pixels y0, y0+1 are final -- a site C or more rows away cannot
+    // bring a value below C^2 >= K_sat -- and are emitted.  Unrolled over S = 0..C-1 (one
+    // rotation) every register index is static and a skipped row pair costs one reset.
+    template <int S>
+    __device__ __forceinline__ void step(int u, uint32_t (&P)[C]) {
         if (u > 0 && (u & 31) == 0) {   // rows u.. start a new batch of 32
             cl = nl;
             cm = nm;
@@ -104,25 +112,36 @@ struct WinState {
         if (__any_sync(0xFFFFFFFFu, (ha < (uint32_t)C) | (hb < (uint32_t)C))) {
             const uint32_t h2a = ha * ha * 0x10001u, h2b = hb * hb * 0x10001u;
 #pragma unroll
-            for (int k = 0; k < C; ++k) {
-                const uint32_t sqa = dsq<C>(2 * k, 0) | (dsq<C>(2 * k + 1, 0) << 16);
-                const uint32_t sqb = dsq<C>(2 * k, 1) | (dsq<C>(2 * k + 1, 1) << 16);
-                const uint32_t prev = (k + 1 < C) ? src[k + 1 < C ? k + 1 : 0] : 0xFFFFFFFFu;
-                dst[k] = __vminu2(prev, __vminu2(sqa + h2a, sqb + h2b));
+            for (int j = 0; j < C; ++j) {
+                const uint32_t sqa = dsq<C>(2 * j, 0) | (dsq<C>(2 * j + 1, 0) << 16);
+                const uint32_t sqb = dsq<C>(2 * j, 1) | (dsq<C>(2 * j + 1, 1) << 16);
+                const int m = (j + S + 1) % C;
+                const uint32_t prev = (j + 1 < C) ? P[m] : 0xFFFFFFFFu;
+                P[m] = __vminu2(prev, __vminu2(sqa + h2a, sqb + h2b));
             }
         } else {
-#pragma unroll
-            for (int k = 0; k < C; ++k) dst[k] = (k + 1 < C) ? src[k + 1 < C ? k + 1 : 0] : 0xFFFFFFFFu;
+            P[S % C] = 0xFFFFFFFFu;   // the new last register starts empty
         }
         const int y0 = u - (C - 1);
-        if (y0 >= 0 && y0 < H) emit(dst[0] & 0xFFFFu);
-        if (y0 + 1 >= 0 && y0 + 1 < H) emit(dst[0] >> 16);
+        const uint32_t v = P[(S + 1) % C];
+        if (y0 >= 0 && y0 < H) emit(v & 0xFFFFu);
+        if (y0 + 1 >= 0 && y0 + 1 < H) emit(v >> 16);
+    }
+
+    template <int S>
+    __device__ __forceinline__ void block(int u0, int total, uint32_t (&P)[C]) {
+        if constexpr (S < C) {
+            if (u0 + 2 * S < total) {
+                step<S>(u0 + 2 * S, P);
+                block<S + 1>(u0, total, P);
+            }
+        }
     }
 };
 
 template <int C>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 4 : 3)) window_kernel(WinParams p) {
-    static_assert(C >= 2 && C <= 64, "window size");
+    static_assert(C >= 2 && C <= 31, "window size (hdist_words reports empty words as 31)");
     __shared__ float lut_s[1025];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) lut_s[i] = p.lut[i];
@@ -149,15 +168,11 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 4 : 3)) window_kern
     st.fetch(32, st.nl, st.nm, st.nr);
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
-    // Two register sets alternate (A -> B -> A) so the per-step shift needs no moves.
-    uint32_t A[C], B[C];
+    uint32_t P[C];
 #pragma unroll
-    for (int k = 0; k < C; ++k) A[k] = 0xFFFFFFFFu;
+    for (int k = 0; k < C; ++k) P[k] = 0xFFFFFFFFu;
     const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
-    for (int u = 0; u < total; u += 4) {
-        st.step(u, A, B);
-        if (u + 2 < total) st.step(u + 2, B, A);
-    }
+    for (int u = 0; u < total; u += 2 * C) st.template block<0>(u, total, P);
 }
 
 }  // namespace ieds
