@@ -151,9 +151,25 @@ int window_size_for(int c) {
     return 0;
 }
 
+size_t window_smem_bytes(int H) { return 4ull * ((H + 2) * ieds::kWinRowWords + 1028); }
+
 template <int C>
 void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp) {
-    ieds::window_kernel<C><<<grid, ieds::kWinWarps * 32, 0, st>>>(wp);
+    ieds::window_kernel<C><<<grid, ieds::kWinWarps * 32, window_smem_bytes(wp.H), st>>>(wp);
+}
+
+template <int C>
+cudaError_t window_attr_t(size_t smem) {
+    return cudaFuncSetAttribute(ieds::window_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t window_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+#define IEDS_WIN_ATTR(c) if (e == cudaSuccess) e = window_attr_t<c>(smem);
+    IEDS_WIN_ATTR(4) IEDS_WIN_ATTR(6) IEDS_WIN_ATTR(8) IEDS_WIN_ATTR(10) IEDS_WIN_ATTR(12) IEDS_WIN_ATTR(14)
+    IEDS_WIN_ATTR(16) IEDS_WIN_ATTR(19) IEDS_WIN_ATTR(22) IEDS_WIN_ATTR(25) IEDS_WIN_ATTR(28) IEDS_WIN_ATTR(31)
+#undef IEDS_WIN_ATTR
+    return e;
 }
 
 void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp) {
@@ -317,7 +333,8 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
         h->c_sat = (int)std::min<int64_t>(cs, 1 << 20);
     }
     h->c_win = window_size_for(std::max(2, h->c_sat));
-    h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT);
+    h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) &&
+                   window_smem_bytes(H) <= (size_t)kMaxSmem;
 
     // frame + (column bitmap for the exact path | two saved rows for the streaming path)
     h->smem_frame = 4ull * (((H + 2) * h->NWP + 3) & ~3) + 8ull * std::max(W, h->NWP);
@@ -337,6 +354,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
+    if (e == cudaSuccess && h->streaming) e = window_attrs(window_smem_bytes(H));
     if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);

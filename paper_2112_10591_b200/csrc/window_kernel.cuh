@@ -21,7 +21,8 @@
 
 namespace ieds {
 
-constexpr int kWinWarps = 8;   // warps (strips) per CTA
+constexpr int kWinWarps = 8;                  // warps (strips) per CTA
+constexpr int kWinRowWords = kWinWarps + 2;   // E_df words of one row a CTA needs (strips +- 1)
 
 struct WinParams {
     const uint32_t* __restrict__ Edf;   // [nb][H][NW+2], word w of row y at 1 + w, zero guards
@@ -61,31 +62,20 @@ __device__ __forceinline__ void st_cs_pred(float* ptr, float v, uint32_t pred) {
 
 template <int C>
 struct WinState {
-    const uint32_t* rp;   // this strip's words of row 0 (words w-1, w, w+1 at rp[0..2])
     int H, NWP2, lane;
-    uint32_t cl, cm, cr, nl, nm, nr;   // current / next batch of 32 rows (lane i = row base+i)
+    uint32_t words_sh;                 // shared address of this strip's words (w-1, w, w+1) of row 0
     float* op;                         // next pixel to emit (rows are emitted in order)
     size_t W;                          // row stride in elements
     uint32_t lut_sh, K_sat, xvalid;
 
-    __device__ __forceinline__ void fetch(int row0, uint32_t& a, uint32_t& m, uint32_t& z) const {
-        const int r = row0 + lane;
-        if (r < H) {
-            const uint32_t* q = rp + (size_t)r * NWP2;
-            a = __ldg(q);
-            m = __ldg(q + 1);
-            z = __ldg(q + 2);
-        } else {
-            a = m = z = 0u;
-        }
-    }
-    __device__ __forceinline__ uint32_t h_of(int src_u) const {
-        int src = src_u;
-        asm volatile("mov.b32 %0, %0;" : "+r"(src));   // one vector copy of the lane index
-        const uint32_t tl = __shfl_sync(0xFFFFFFFFu, cl, src);
-        const uint32_t t = __shfl_sync(0xFFFFFFFFu, cm, src);
-        const uint32_t tr = __shfl_sync(0xFFFFFFFFu, cr, src);
-        return (uint32_t)hdist_words(tl, t, tr, lane);   // <= 32; >= C contributes >= C^2
+    // h of row u for this lane: 3 broadcast shared loads (words w-1, w, w+1 of the row)
+    __device__ __forceinline__ uint32_t h_of(int u) const {
+        const uint32_t a = words_sh + (uint32_t)min(u, H) * (4u * kWinRowWords);
+        uint32_t tl, t, tr;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tl) : "r"(a));
+        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(t) : "r"(a));
+        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(tr) : "r"(a));
+        return (uint32_t)hdist_words(tl, t, tr, lane);   // <= 31; >= C contributes >= C^2
     }
     __device__ __forceinline__ void emit(uint32_t v) {
         const float f = lds_f32(lut_sh + 4u * min(v, K_sat));
@@ -102,13 +92,7 @@ struct WinState {
     // rotation) every register index is static and a skipped row pair costs one reset.
     template <int S>
     __device__ __forceinline__ void step(int u, uint32_t (&P)[C]) {
-        if (u > 0 && (u & 31) == 0) {   // rows u.. start a new batch of 32
-            cl = nl;
-            cm = nm;
-            cr = nr;
-            fetch(u + 32, nl, nm, nr);
-        }
-        const uint32_t ha = h_of(u & 31), hb = h_of((u & 31) + 1);   // rows >= H: no site
+        const uint32_t ha = h_of(u), hb = h_of(u + 1);   // rows >= H are zero words: no site
         if (__any_sync(0xFFFFFFFFu, (ha < (uint32_t)C) | (hb < (uint32_t)C))) {
             const uint32_t h2a = ha * ha * 0x10001u, h2b = hb * hb * 0x10001u;
 #pragma unroll
@@ -140,22 +124,32 @@ struct WinState {
 };
 
 template <int C>
-__global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 4 : 3)) window_kernel(WinParams p) {
+__global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
     static_assert(C >= 2 && C <= 31, "window size (hdist_words reports empty words as 31)");
-    __shared__ float lut_s[1025];
+    extern __shared__ __align__(16) uint32_t wsm[];   // [H + 2][kWinRowWords] E_df words, then the table
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
+    const int NWP2 = p.NW + 2;
+    // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
+    // plus two zero rows past the end for the row pair straddling H
+    {
+        const uint32_t* src = p.Edf + (size_t)b * H * NWP2 + w0;
+        const int n = (H + 2) * kWinRowWords;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int y = i / kWinRowWords, c = i - y * kWinRowWords;
+            wsm[i] = (y < H && w0 + c < NWP2) ? __ldg(src + (size_t)y * NWP2 + c) : 0u;
+        }
+    }
+    float* lut_s = reinterpret_cast<float*>(wsm + (H + 2) * kWinRowWords);
     for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) lut_s[i] = p.lut[i];
     __syncthreads();
 
-    const int w = blockIdx.x * kWinWarps + warp;
+    const int w = w0 + warp;
     if (w >= p.NW) return;
-    const int b = blockIdx.y;
-    const int H = p.H;
     const int x = 32 * w + lane;
     WinState<C> st;
-    st.rp = p.Edf + (size_t)b * H * (p.NW + 2) + w;
     st.H = H;
-    st.NWP2 = p.NW + 2;
+    st.NWP2 = NWP2;
     st.lane = lane;
     st.W = (size_t)p.W;
     st.xvalid = x < p.W ? 1u : 0u;
@@ -164,8 +158,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 4 : 3)) window_kern
     uint32_t lut_sh = (uint32_t)__cvta_generic_to_shared(lut_s);
     asm volatile("" : "+r"(lut_sh));   // keep the shared address in a register
     st.lut_sh = lut_sh;
-    st.fetch(0, st.cl, st.cm, st.cr);
-    st.fetch(32, st.nl, st.nm, st.nr);
+    st.words_sh = (uint32_t)__cvta_generic_to_shared(wsm + warp);
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
     uint32_t P[C];
