@@ -153,8 +153,14 @@ __device__ __forceinline__ void denoise_fill_inplace(uint32_t* fr, uint32_t* sv,
     const size_t NW2 = (size_t)p.NW + 2;
     uint32_t* scratch = p.Edf_scratch + (size_t)b * H * NW2;
     const int n = H * NWP;
-    for (int j = tid; j < n; j += nthr) {
-        const int y = j / NWP, w = j - y * NWP;
+    // (y, w) of index j advanced incrementally (no division in the loop)
+    const int dy = nthr / NWP, dw = nthr - (nthr / NWP) * NWP;
+    int y = tid / NWP, w = tid - (tid / NWP) * NWP;
+    for (int j = tid; j < n; j += nthr, y += dy, w += dw) {
+        if (w >= NWP) {
+            w -= NWP;
+            ++y;
+        }
         if (w >= p.NW) continue;
         const int i = j + NWP;
         const uint32_t c = fr[i];
