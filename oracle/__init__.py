@@ -49,6 +49,8 @@ def _load():
             lib.oracle_edt_separable.argtypes = [P, i32, i32, P]
             lib.oracle_edt_bruteforce.argtypes = [P, i32, i32, P]
             lib.oracle_surface.argtypes = [P, i64, f64, P]
+            lib.oracle_transfer.argtypes = [P, i64, i32, f64, f64, P]
+            lib.oracle_quantize_u8.argtypes = [P, i64, P]
             lib.oracle_alpha_from_dsat.argtypes = [f64]
             lib.oracle_alpha_from_dsat.restype = f64
             lib.oracle_build_window.argtypes = [P, i64, i32, i32, i32, i32, f64, P, P, P, P, P]
@@ -112,6 +114,25 @@ def surface(D2, alpha: float) -> np.ndarray:
     out = np.empty(D2.shape, np.float64)
     _load().oracle_surface(_ptr(D2), D2.size, float(alpha), _ptr(out))
     return out
+
+
+TRANSFERS = {"invexp": 0, "linear": 1, "bounded": 2, "log": 3}
+
+
+def transfer(D2, kind: str, alpha: float = 1.0, bound: float = 6.0) -> np.ndarray:
+    """Ablation transfers of §IV-D: invexp (Eq. (1)), linear, bounded, log."""
+    D2 = np.ascontiguousarray(D2, dtype=np.int64)
+    out = np.empty(D2.shape, np.float64)
+    _load().oracle_transfer(_ptr(D2), D2.size, TRANSFERS[kind], float(alpha), float(bound), _ptr(out))
+    return out
+
+
+def quantize_u8(S) -> np.ndarray:
+    """8-bit coding q = round(255 * d_exp), half away from zero."""
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    q = np.empty(S.shape, np.uint8)
+    _load().oracle_quantize_u8(_ptr(S), S.size, _ptr(q))
+    return q
 
 
 def alpha_from_dsat(d_sat: float) -> float:

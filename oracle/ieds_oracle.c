@@ -222,6 +222,43 @@ void oracle_surface(const int64_t *D2, int64_t n, double alpha, double *S)
     }
 }
 
+/* ---- Ablation transfers of §IV-D (Fig. 4) --------------------------
+ *   kind 0: Eq. (1) inverse exponential  1 - exp(-d/alpha)           (proposed)
+ *   kind 1: linear distance transform    Id(d) = d                   (Ours_DS_L,  P:306)
+ *   kind 2: upper-bounded                min(d, bound), bound = 6 px (Ours_DS_LB)
+ *   kind 3: logarithmic                  ln(d + 1)                   (Ours_DS_Log)
+ * d = sqrt(D2) in pixels.  An empty frame (D2 = ORACLE_NO_EDGE) is the limit d -> inf:
+ * 1 for kind 0, bound for kind 2, +inf for kinds 1 and 3 (reading R14 in DESIGN.md). */
+void oracle_transfer(const int64_t *D2, int64_t n, int kind, double alpha, double bound, double *out)
+{
+    for (int64_t i = 0; i < n; i++) {
+        if (D2[i] == ORACLE_NO_EDGE) {
+            out[i] = (kind == 0) ? 1.0 : (kind == 2) ? bound : HUGE_VAL;
+            continue;
+        }
+        double d = sqrt((double)D2[i]);
+        switch (kind) {
+            case 0: out[i] = 1.0 - exp(-d / alpha); break;
+            case 1: out[i] = d; break;
+            case 2: out[i] = d < bound ? d : bound; break;
+            default: out[i] = log(d + 1.0); break;
+        }
+    }
+}
+
+/* ---- 8-bit coding of the surface ("coded on 8 bits (values ranging from 0 to 1 are
+ * represented by values between 0 and 255)"): q = round(255 * d_exp), half away from zero
+ * (d_exp >= 0, so floor(255 * d_exp + 0.5)); reading R15. */
+void oracle_quantize_u8(const double *S, int64_t n, uint8_t *q)
+{
+    for (int64_t i = 0; i < n; i++) {
+        double v = floor(255.0 * S[i] + 0.5);
+        if (v < 0.0) v = 0.0;
+        if (v > 255.0) v = 255.0;
+        q[i] = (uint8_t)v;
+    }
+}
+
 /* ---- Eq. (2)-(3): alpha = -d_sat / ln(eps), eps = 1/255 --------------------
  * The paper prints alpha ~ d_sat / 5.541, i.e. ln 255 = 5.5413; the oracle keeps
  * the full-precision ln (reading R6).  d_sat <= 0 (or NaN) returns NaN. */

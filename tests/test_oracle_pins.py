@@ -282,3 +282,34 @@ def test_build_window_composes_steps():
     offs = np.array([0, len(xy), len(xy2)])
     res = oracle.build_batch(xy2, offs, c.width, c.height, wl.n_d, wl.n_f, a, threads=2)
     assert np.array_equal(res[0]["S"], out["S"])
+
+
+# ---------------------------------------------------------------- §IV-D ablations, 8-bit coding
+
+def test_transfer_variants_fig4():
+    # Fig. 4 / §IV-D: Id(x), min(x, 6), ln(x + 1), 1 - exp(-x/alpha)
+    D2 = np.array([0, 1, 25, 36, 49, 100, oracle.NO_EDGE])
+    d = np.array([0.0, 1.0, 5.0, 6.0, 7.0, 10.0])
+    lin = oracle.transfer(D2, "linear")
+    assert np.array_equal(lin[:6], d) and np.isinf(lin[6])            # 3-4-5 -> 5 etc.
+    bnd = oracle.transfer(D2, "bounded", bound=6.0)
+    assert np.array_equal(bnd, [0, 1, 5, 6, 6, 6, 6])                  # upper bound 6 px
+    lg = oracle.transfer(D2, "log")
+    assert lg[0] == 0.0 and abs(lg[1] - math.log(2.0)) < 1e-15 and np.isinf(lg[6])
+    assert abs(lg[2] - math.log(6.0)) < 1e-15
+    a = oracle.alpha_from_dsat(6.0)
+    assert np.array_equal(oracle.transfer(D2, "invexp", alpha=a), oracle.surface(D2, a))
+    # all variants are 0 on edge pixels and monotone non-decreasing in the distance
+    big = np.arange(0, 3000, dtype=np.int64)
+    for k in ("linear", "bounded", "log", "invexp"):
+        v = oracle.transfer(big, k, alpha=a)
+        assert v[0] == 0.0 and np.all(np.diff(v) >= 0)
+
+
+def test_quantize_u8_saturation():
+    # 8-bit coding: q(d_sat) = 254, q(d_sat + 1) = 255 for d_sat = 6; q(0) = 0
+    a = oracle.alpha_from_dsat(6.0)
+    q = oracle.quantize_u8(oracle.surface(np.array([0, 36, 49, oracle.NO_EDGE]), a))
+    assert list(q) == [0, 254, 255, 255]
+    # round half away from zero: 0.5/255 -> 1, just below -> 0
+    assert list(oracle.quantize_u8(np.array([0.5 / 255.0, 0.49 / 255.0, 1.0]))) == [1, 0, 255]
