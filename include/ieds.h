@@ -12,6 +12,9 @@
  *       as an exact integer squared distance D2;
  *   a5  surface S = 1 - exp(-sqrt(D2) / alpha) (Eq. (1)), fp32.
  * A window whose E_df is empty has D2 = IEDS_NO_EDGE everywhere and S = 1 (saturated).
+ * Row f1 variants (config.transfer / config.out_format): the ablation transfers of §IV-D
+ * (Fig. 4) -- Id(d), min(d, bound), ln(d + 1) -- and the 8-bit coding of the
+ * surface, q = round(255 * S) half away from zero.
  * alpha may be derived from the saturation distance with ieds_alpha_from_dsat (Eq. (2)-(3),
  * P:228-233).
  *
@@ -22,7 +25,7 @@
  *                   events of window b are events_xy[window_offsets[b] .. window_offsets[b+1]).
  *   window_offsets  int64 [num_windows + 1], offsets[0] >= 0, non-decreasing,
  *                   offsets[num_windows] <= n_events; empty windows are allowed.
- *   surfaces        float32 [num_windows][height][width], row-major.
+ *   surfaces        float32 [num_windows][height][width], row-major (uint8 with IEDS_OUT_U8).
  *   *_bits          uint32 [num_windows][height][ceil(width/32)]: bit (x % 32) of word x/32
  *                   is pixel x (LSB = lowest x); padding bits beyond width are 0.
  *   sqdist          uint32 [num_windows][height][width]: exact D2, IEDS_NO_EDGE if the
@@ -71,7 +74,20 @@ typedef struct {
                             /* batches of any size are processed chunk by chunk. 0 = 128 */
     int32_t device;         /* CUDA device ordinal; -1 = current device                 */
     int32_t flags;          /* IEDS_FLAG_* bits                                          */
+    int32_t transfer;       /* IEDS_TRANSFER_*; 0 = Eq. (1)                             */
+    double bound;           /* IEDS_TRANSFER_BOUNDED: upper bound in pixels (> 0) */
+    int32_t out_format;     /* IEDS_OUT_F32 (0) or IEDS_OUT_U8 (1, Eq. (1) only)         */
 } ieds_config;
+
+/* transfer of the distance d = sqrt(D2) (pixels); an empty frame is the limit d -> inf */
+#define IEDS_TRANSFER_INVEXP 0  /* 1 - exp(-d / alpha), Eq. (1); empty -> 1        */
+#define IEDS_TRANSFER_LINEAR 1  /* Id(d); empty -> +inf                              */
+#define IEDS_TRANSFER_BOUNDED 2 /* min(d, bound); empty -> bound                     */
+#define IEDS_TRANSFER_LOG 3     /* ln(d + 1); empty -> +inf                          */
+#define IEDS_OUT_F32 0          /* float32 surfaces                                          */
+#define IEDS_OUT_U8 1           /* uint8 q = round(255 * S), half away from zero;    */
+                                /* requires IEDS_TRANSFER_INVEXP and q saturating (255) for  */
+                                /* some D2 <= 1024                                            */
 
 /* Always run the uncapped exact-EDT kernel.  By default, when sqdist is not requested and
  * the saturation radius c = ceil(sqrt(K_sat)) is <= 31 pixels, the surface is produced by
@@ -92,7 +108,7 @@ void ieds_destroy(ieds_handle *h);
  * synchronisation and no allocation: the call is CUDA-graph capturable.  num_windows = 0
  * is a no-op. */
 int ieds_build_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *window_offsets,
-                     int64_t n_events, int32_t num_windows, float *surfaces, uint32_t *edge_bits,
+                     int64_t n_events, int32_t num_windows, void *surfaces, uint32_t *edge_bits,
                      uint32_t *denoised_bits, uint32_t *filtered_bits, uint32_t *sqdist,
                      void *stream);
 
@@ -102,7 +118,7 @@ int ieds_build_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *w
  * Page-locked host buffers give full PCIe bandwidth.  Grows internal buffers as needed
  * (this entry point may allocate).  Returns data errors directly (no ieds_sync needed). */
 int ieds_build_batch_host(ieds_handle *h, const uint32_t *events_xy,
-                          const int64_t *window_offsets, int32_t num_windows, float *surfaces);
+                          const int64_t *window_offsets, int32_t num_windows, void *surfaces);
 
 /* Wait for `stream`, then return (and clear) the latched device error, or IEDS_OK. */
 int ieds_sync(ieds_handle *h, void *stream);

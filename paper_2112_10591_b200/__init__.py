@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 
-from ._lib import (IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
+from ._lib import (IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, OUT_FORMATS, TRANSFERS, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
                    check, load)
 
 __all__ = ["Builder", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
@@ -45,13 +45,16 @@ class Builder:
     """One ieds_handle on one CUDA device.
 
     Builder(width, height, n_d, n_f, alpha=None, d_sat=6.0) -- alpha defaults to
-    alpha_from_dsat(d_sat).  exact_edt=True forces the uncapped exact-EDT kernel even when
+    alpha_from_dsat(d_sat).  transfer selects Eq. (1) ("invexp") or a §IV-D ablation ("linear",
+    "bounded" with `bound`, "log"); out="u8" gives the 8-bit coded surface.
+    exact_edt=True forces the uncapped exact-EDT kernel even when
     only surfaces are requested (the default streaming kernel gives bit-identical surfaces).  build_batch() enqueues on the current torch stream (or the
     given one) and does not synchronise; sync() reports latched device errors.
     """
 
     def __init__(self, width: int, height: int, n_d: int, n_f: int, alpha: float | None = None,
-                 d_sat: float = 6.0, chunk_windows: int = 0, device=None, exact_edt: bool = False):
+                 d_sat: float = 6.0, chunk_windows: int = 0, device=None, exact_edt: bool = False,
+                 transfer: str = "invexp", bound: float = 6.0, out: str = "f32"):
         import torch
 
         if not torch.cuda.is_available():
@@ -62,8 +65,13 @@ class Builder:
         if alpha is None:
             alpha = alpha_from_dsat(d_sat)
         self.params = Params(width, height, n_d, n_f, float(alpha))
+        if transfer not in TRANSFERS or out not in OUT_FORMATS:
+            raise ValueError(f"transfer must be one of {list(TRANSFERS)}, out one of {list(OUT_FORMATS)}")
         cfg = IedsConfig(width, height, n_d, n_f, float(alpha), chunk_windows, self.device.index,
-                         IEDS_FLAG_EXACT_EDT if exact_edt else 0)
+                         IEDS_FLAG_EXACT_EDT if exact_edt else 0, TRANSFERS[transfer], float(bound),
+                         OUT_FORMATS[out])
+        self.out = out
+        self.transfer = transfer
         self.exact_edt = exact_edt
         h = ctypes.c_void_p()
         check(load().ieds_create(ctypes.byref(cfg), ctypes.byref(h)), "ieds_create")
@@ -137,9 +145,10 @@ class Builder:
         self._check_dev(events_xy, "events_xy", u32)
         self._check_dev(offsets, "offsets", (torch.int64,))
         B = offsets.numel() - 1
+        odt = torch.uint8 if self.out == "u8" else torch.float32
         if out is None:
-            out = torch.empty((B, self.height, self.width), dtype=torch.float32, device=self.device)
-        self._check_dev(out, "out", (torch.float32,))
+            out = torch.empty((B, self.height, self.width), dtype=odt, device=self.device)
+        self._check_dev(out, "out", (odt,))
         if out.numel() < B * self.height * self.width:
             raise ValueError("out too small")
         for name, t, n in (("edge_bits", edge_bits, self.words), ("denoised_bits", denoised_bits, self.words),
@@ -164,10 +173,11 @@ class Builder:
         xy = np.ascontiguousarray(events_xy).view(np.uint32)
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         B = len(off) - 1
+        odt = np.uint8 if self.out == "u8" else np.float32
         if out is None:
-            out = np.empty((B, self.height, self.width), np.float32)
-        if out.dtype != np.float32 or not out.flags.c_contiguous or out.size < B * self.height * self.width:
-            raise ValueError("out must be a C-contiguous float32 array of B*H*W")
+            out = np.empty((B, self.height, self.width), odt)
+        if out.dtype != odt or not out.flags.c_contiguous or out.size < B * self.height * self.width:
+            raise ValueError(f"out must be a C-contiguous {np.dtype(odt).name} array of B*H*W")
         check(load().ieds_build_batch_host(self._h, xy.ctypes.data_as(ctypes.c_void_p),
                                            off.ctypes.data_as(ctypes.c_void_p), B,
                                            out.ctypes.data_as(ctypes.c_void_p)), "ieds_build_batch_host")

@@ -38,10 +38,15 @@ class IedsConfig(ctypes.Structure):
         ("chunk_windows", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+        ("transfer", ctypes.c_int32),
+        ("bound", ctypes.c_double),
+        ("out_format", ctypes.c_int32),
     ]
 
 
 IEDS_FLAG_EXACT_EDT = 1
+TRANSFERS = {"invexp": 0, "linear": 1, "bounded": 2, "log": 3}   # IEDS_TRANSFER_*
+OUT_FORMATS = {"f32": 0, "u8": 1}                                  # IEDS_OUT_*
 
 
 class IedsError(RuntimeError):

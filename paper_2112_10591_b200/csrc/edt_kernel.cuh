@@ -24,11 +24,13 @@ struct EdtParams {
     const uint32_t* __restrict__ T;                // [nb][NR][W]
     const unsigned long long* __restrict__ colmask;  // [nb][W]
     int W, H, NR, NS, SEGW;
-    float* __restrict__ S;                          // [nb][H][W]
+    void* __restrict__ S;                           // [nb][H][W] float32, or uint8 if out_u8
     uint32_t* __restrict__ D2;                      // [nb][H][W] or null
     const float* __restrict__ lut;                  // [K_lut]
     int K_lut, K_sat;
     float c_exp;                                    // -log2(e) / alpha
+    int transfer, out_u8;                           // IEDS_TRANSFER_*, IEDS_OUT_U8
+    float bound, sat_value, empty_value;            // saturated value (D2 >= K_sat), empty frame
 };
 
 struct SmemLayout {
@@ -101,6 +103,22 @@ __device__ __forceinline__ bool dominated(const Ent& p, const Ent& q, const Ent&
     const long long kq = (long long)q.f + (long long)q.site * q.site;
     const long long kr = (long long)r.f + (long long)r.site * r.site;
     return (kq - kp) * (long long)(r.site - q.site) >= (kr - kq) * (long long)(q.site - p.site);
+}
+
+// transfer of an exact squared distance (Eq. (1) or a §IV-D ablation, see ieds.h): the
+// fp64-built table below K_lut, the saturated value from K_sat, fp32 arithmetic in between
+// (only reached for large alpha / unbounded transfers)
+__device__ __forceinline__ float transfer_value(uint32_t d2, const float* lut, const EdtParams& p) {
+    if (d2 < (uint32_t)p.K_lut) return lut[d2];
+    if (d2 == 0xFFFFFFFFu) return p.empty_value;
+    if (d2 >= (uint32_t)p.K_sat) return p.sat_value;
+    const float d = sqrtf((float)d2);   // d2 < 2^24: exact input, correctly rounded
+    switch (p.transfer) {
+        case 0: return 1.0f - exp2f(p.c_exp * d);
+        case 1: return d;
+        case 2: return fminf(d, p.bound);
+        default: return log1pf(d);
+    }
 }
 
 __device__ __forceinline__ int envF(int x, const Ent& e) {
@@ -229,7 +247,8 @@ __global__ void __launch_bounds__(512) edt_kernel(EdtParams p) {
 
     // ---- phase 3: evaluate D2 on each segment by walking the merged envelope; write S
     const size_t plane = (size_t)p.H * W;
-    float* Sb = p.S + (size_t)b * plane;
+    float* Sb = reinterpret_cast<float*>(p.S) + (size_t)b * plane;
+    uint8_t* Qb = reinterpret_cast<uint8_t*>(p.S) + (size_t)b * plane;
     uint32_t* Db = p.D2 ? p.D2 + (size_t)b * plane : nullptr;
     for (int s = warp; s < NS; s += nwarps) {
         const int a_s = s * SEGW, b_s = min(W, a_s + SEGW);
@@ -261,10 +280,7 @@ __global__ void __launch_bounds__(512) edt_kernel(EdtParams p) {
                 }
                 d2 = (uint32_t)envF(x, cur);
             }
-            float v;
-            if (d2 < (uint32_t)p.K_lut) v = sm.lut[d2];
-            else if (d2 >= (uint32_t)p.K_sat) v = 1.0f;
-            else v = 1.0f - exp2f(p.c_exp * sqrtf((float)d2));
+            const float v = transfer_value(d2, sm.lut, p);
             const int c = (x - a_s) & 7;
             stg[lane * 9 + c] = v;
             if (Db) stgd[lane * 9 + c] = d2;
@@ -276,7 +292,8 @@ __global__ void __launch_bounds__(512) edt_kernel(EdtParams p) {
                     const int row = 4 * k + (lane >> 3), col = lane & 7;
                     const int y = y0 + row;
                     if (y < p.H && col <= c) {
-                        Sb[(size_t)y * W + xb + col] = stg[row * 9 + col];
+                        if (p.out_u8) Qb[(size_t)y * W + xb + col] = (uint8_t)stg[row * 9 + col];
+                        else Sb[(size_t)y * W + xb + col] = stg[row * 9 + col];
                         if (Db) Db[(size_t)y * W + xb + col] = stgd[row * 9 + col];
                     }
                 }

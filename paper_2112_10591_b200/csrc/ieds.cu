@@ -35,7 +35,7 @@ struct HostPath {
     cudaEvent_t kdone[2] = {nullptr, nullptr};   // chunk's kernels finished (scratch free)
     uint32_t* d_xy[2] = {nullptr, nullptr};
     int64_t* d_off[2] = {nullptr, nullptr};
-    float* d_S[2] = {nullptr, nullptr};
+    float* d_S[2] = {nullptr, nullptr};   // (uint8 surfaces use the same buffers)
     int64_t* h_off[2] = {nullptr, nullptr};   // pinned, rebased offsets
     int64_t cap_ev[2] = {0, 0};
 };
@@ -92,17 +92,45 @@ size_t edt_smem_bytes(int W, int NS, int SEGW, int K_lut, bool d2) {
 }
 
 // fp32 value of Eq. (1) rounded from fp64, and the first D2 at which it is exactly 1.0f
-float surface_f32(double d2, double alpha) { return (float)(1.0 - std::exp(-std::sqrt(d2) / alpha)); }
+// Value stored for integer D2 (fp64 arithmetic, then rounded to the output type): the
+// transfer of d = sqrt(D2) (Eq. (1) or a §IV-D ablation), 8-bit coded if out_u8.
+double transfer_f64(int transfer, double d2, double alpha, double bound) {
+    const double d = std::sqrt(d2);
+    switch (transfer) {
+        case IEDS_TRANSFER_INVEXP: return 1.0 - std::exp(-d / alpha);
+        case IEDS_TRANSFER_LINEAR: return d;
+        case IEDS_TRANSFER_BOUNDED: return std::min(d, bound);
+        default: return std::log(d + 1.0);
+    }
+}
 
-int64_t saturation_index(double alpha) {
+float table_value(const ieds_config& c, double d2) {
+    const double v = transfer_f64(c.transfer, d2, c.alpha, c.bound);
+    if (c.out_format == IEDS_OUT_U8) return (float)std::min(255.0, std::max(0.0, std::floor(255.0 * v + 0.5)));
+    return (float)v;
+}
+
+// value of the limit D2 -> inf (saturation; also the value of an empty frame), or +inf
+float limit_value(const ieds_config& c) {
+    switch (c.transfer) {
+        case IEDS_TRANSFER_INVEXP: return c.out_format == IEDS_OUT_U8 ? 255.0f : 1.0f;
+        case IEDS_TRANSFER_BOUNDED: return (float)c.bound;
+        default: return INFINITY;
+    }
+}
+
+// first integer D2 whose stored value equals the limit (values are monotone in D2), or 2^40
+int64_t saturation_index(const ieds_config& c) {
+    const float lim = limit_value(c);
+    if (std::isinf(lim)) return 1ll << 40;
     int64_t lo = 0, hi = 1;
-    while (surface_f32((double)hi, alpha) != 1.0f) {
+    while (table_value(c, (double)hi) != lim) {
         hi *= 2;
         if (hi > (1ll << 40)) return hi;
     }
-    while (lo < hi) {   // first D2 with value 1.0f (the value is monotone in D2)
+    while (lo < hi) {
         int64_t mid = lo + (hi - lo) / 2;
-        if (surface_f32((double)mid, alpha) == 1.0f) hi = mid;
+        if (table_value(c, (double)mid) == lim) hi = mid;
         else lo = mid + 1;
     }
     return lo;
@@ -154,13 +182,19 @@ int window_size_for(int c) {
 size_t window_smem_bytes(int H) { return 4ull * ((H + 2) * ieds::kWinRowWords + 1028); }
 
 template <int C>
-void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp) {
-    ieds::window_kernel<C><<<grid, ieds::kWinWarps * 32, window_smem_bytes(wp.H), st>>>(wp);
+void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, bool u8) {
+    if (u8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, window_smem_bytes(wp.H), st>>>(wp);
+    else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, window_smem_bytes(wp.H), st>>>(wp);
 }
 
 template <int C>
 cudaError_t window_attr_t(size_t smem) {
-    return cudaFuncSetAttribute(ieds::window_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(ieds::window_kernel<C, float>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ieds::window_kernel<C, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+    return e;
 }
 
 cudaError_t window_attrs(size_t smem) {
@@ -172,25 +206,27 @@ cudaError_t window_attrs(size_t smem) {
     return e;
 }
 
-void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp) {
+void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp, bool u8) {
     switch (C) {
-        case 4: launch_window_t<4>(grid, st, wp); break;
-        case 6: launch_window_t<6>(grid, st, wp); break;
-        case 8: launch_window_t<8>(grid, st, wp); break;
-        case 10: launch_window_t<10>(grid, st, wp); break;
-        case 12: launch_window_t<12>(grid, st, wp); break;
-        case 14: launch_window_t<14>(grid, st, wp); break;
-        case 16: launch_window_t<16>(grid, st, wp); break;
-        case 19: launch_window_t<19>(grid, st, wp); break;
-        case 22: launch_window_t<22>(grid, st, wp); break;
-        case 25: launch_window_t<25>(grid, st, wp); break;
-        case 28: launch_window_t<28>(grid, st, wp); break;
-        default: launch_window_t<31>(grid, st, wp); break;
+        case 4: launch_window_t<4>(grid, st, wp, u8); break;
+        case 6: launch_window_t<6>(grid, st, wp, u8); break;
+        case 8: launch_window_t<8>(grid, st, wp, u8); break;
+        case 10: launch_window_t<10>(grid, st, wp, u8); break;
+        case 12: launch_window_t<12>(grid, st, wp, u8); break;
+        case 14: launch_window_t<14>(grid, st, wp, u8); break;
+        case 16: launch_window_t<16>(grid, st, wp, u8); break;
+        case 19: launch_window_t<19>(grid, st, wp, u8); break;
+        case 22: launch_window_t<22>(grid, st, wp, u8); break;
+        case 25: launch_window_t<25>(grid, st, wp, u8); break;
+        case 28: launch_window_t<28>(grid, st, wp, u8); break;
+        default: launch_window_t<31>(grid, st, wp, u8); break;
     }
 }
 
+size_t out_elem_bytes(const ieds_handle* h) { return h->cfg.out_format == IEDS_OUT_U8 ? 1 : 4; }
+
 int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int64_t n_events, int nb,
-                 float* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st) {
+                 void* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st) {
     ieds::FrameParams fp;
     fp.xy = xy;
     fp.offsets = offsets;
@@ -234,7 +270,7 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
         dim3 wgrid((h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps, nb);
         prof_pair(h, 1, &pa, &pb);
         if (pa) cudaEventRecord(pa, st);
-        launch_window(h->c_win, wgrid, st, wp);
+        launch_window(h->c_win, wgrid, st, wp, h->cfg.out_format == IEDS_OUT_U8);
         if (pb) cudaEventRecord(pb, st);
         cudaError_t e2 = cudaGetLastError();
         return e2 == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
@@ -254,6 +290,11 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     ep.K_lut = h->K_lut;
     ep.K_sat = h->K_sat;
     ep.c_exp = h->c_exp;
+    ep.transfer = h->cfg.transfer;
+    ep.out_u8 = h->cfg.out_format == IEDS_OUT_U8;
+    ep.bound = (float)h->cfg.bound;
+    ep.sat_value = limit_value(h->cfg);
+    ep.empty_value = limit_value(h->cfg);
     dim3 grid(h->NR, nb);
     prof_pair(h, 1, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
@@ -296,6 +337,13 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (cfg->n_d < 0 || cfg->n_d > 4 || cfg->n_f < 1 || cfg->n_f > 5) return IEDS_EINVAL;
     if (!(cfg->alpha > 0.0) || !std::isfinite(cfg->alpha)) return IEDS_EINVAL;
     if (cfg->chunk_windows < 0 || (cfg->flags & ~IEDS_FLAG_EXACT_EDT)) return IEDS_EINVAL;
+    if (cfg->transfer < IEDS_TRANSFER_INVEXP || cfg->transfer > IEDS_TRANSFER_LOG) return IEDS_EINVAL;
+    if (cfg->transfer == IEDS_TRANSFER_BOUNDED && !(cfg->bound > 0.0 && std::isfinite(cfg->bound)))
+        return IEDS_EINVAL;
+    if (cfg->out_format != IEDS_OUT_F32 && cfg->out_format != IEDS_OUT_U8) return IEDS_EINVAL;
+    if (cfg->out_format == IEDS_OUT_U8 &&
+        (cfg->transfer != IEDS_TRANSFER_INVEXP || saturation_index(*cfg) > kLutMax))
+        return IEDS_EINVAL;
 
     ieds_handle* h = new ieds_handle();
     h->cfg = *cfg;
@@ -321,7 +369,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->SEGW = segw;
 
     const double alpha = cfg->alpha;
-    int64_t ksat = saturation_index(alpha);
+    int64_t ksat = saturation_index(*cfg);
     if (ksat > (1ll << 31)) ksat = (1ll << 31);
     h->K_sat = (int)std::min<int64_t>(ksat, 0x7FFFFFFF);
     h->K_lut = (int)std::min<int64_t>(ksat, kLutMax);
@@ -366,8 +414,8 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (e == cudaSuccess) e = cudaMalloc(&h->lut, sizeof(float) * (h->K_lut + 1));
     if (e == cudaSuccess) {
         std::vector<float> lut(h->K_lut + 1);
-        for (int i = 0; i < h->K_lut; ++i) lut[i] = surface_f32((double)i, alpha);
-        lut[h->K_lut] = 1.0f;
+        for (int i = 0; i < h->K_lut; ++i) lut[i] = table_value(*cfg, (double)i);
+        lut[h->K_lut] = limit_value(*cfg);
         e = cudaMemcpy(h->lut, lut.data(), sizeof(float) * lut.size(), cudaMemcpyHostToDevice);
     }
     if (e != cudaSuccess) {
@@ -429,12 +477,13 @@ int64_t ieds_launches_per_batch(const ieds_handle* h, int32_t num_windows) {
 }
 
 int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* window_offsets,
-                     int64_t n_events, int32_t num_windows, float* surfaces, uint32_t* edge_bits,
+                     int64_t n_events, int32_t num_windows, void* surfaces, uint32_t* edge_bits,
                      uint32_t* denoised_bits, uint32_t* filtered_bits, uint32_t* sqdist, void* stream) {
     if (!h || num_windows < 0 || n_events < 0) return IEDS_EINVAL;
     if (num_windows == 0) return IEDS_OK;
     if (!surfaces || !window_offsets || (n_events > 0 && !events_xy)) return IEDS_EINVAL;
-    if ((reinterpret_cast<uintptr_t>(events_xy) & 3u) || (reinterpret_cast<uintptr_t>(surfaces) & 3u))
+    if ((reinterpret_cast<uintptr_t>(events_xy) & 3u) ||
+        (reinterpret_cast<uintptr_t>(surfaces) & (out_elem_bytes(h) - 1)))
         return IEDS_EINVAL;
     DeviceGuard g(h->dev);
     if (!g.ok) return IEDS_ECUDA;
@@ -443,7 +492,8 @@ int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* w
     const size_t bplane = (size_t)h->NW * h->cfg.height;
     for (int c0 = 0; c0 < num_windows; c0 += h->chunk) {
         const int nb = std::min(h->chunk, num_windows - c0);
-        int rc = launch_chunk(h, events_xy, window_offsets + c0, n_events, nb, surfaces + c0 * plane,
+        int rc = launch_chunk(h, events_xy, window_offsets + c0, n_events, nb,
+                              static_cast<char*>(surfaces) + c0 * plane * out_elem_bytes(h),
                               edge_bits ? edge_bits + c0 * bplane : nullptr,
                               denoised_bits ? denoised_bits + c0 * bplane : nullptr,
                               filtered_bits ? filtered_bits + c0 * bplane : nullptr,
@@ -468,7 +518,7 @@ int ieds_sync(ieds_handle* h, void* stream) {
 }
 
 int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64_t* window_offsets,
-                          int32_t num_windows, float* surfaces) {
+                          int32_t num_windows, void* surfaces) {
     if (!h || num_windows < 0) return IEDS_EINVAL;
     if (num_windows == 0) return IEDS_OK;
     if (!window_offsets || !surfaces) return IEDS_EINVAL;
@@ -485,7 +535,7 @@ int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64
         if (!hp.st[i]) e = cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking);
         if (e == cudaSuccess && !hp.done[i]) e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming);
         if (e == cudaSuccess && !hp.kdone[i]) e = cudaEventCreateWithFlags(&hp.kdone[i], cudaEventDisableTiming);
-        if (e == cudaSuccess && !hp.d_S[i]) e = cudaMalloc(&hp.d_S[i], sizeof(float) * plane * chunk);
+        if (e == cudaSuccess && !hp.d_S[i]) e = cudaMalloc(&hp.d_S[i], sizeof(float) * plane * chunk);   // fits u8
         if (e == cudaSuccess && !hp.d_off[i]) e = cudaMalloc(&hp.d_off[i], sizeof(int64_t) * (chunk + 1));
         if (e == cudaSuccess && !hp.h_off[i]) e = cudaMallocHost(&hp.h_off[i], sizeof(int64_t) * (chunk + 1));
     }
@@ -523,8 +573,8 @@ int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64
         if (rc != IEDS_OK) return rc;
         e = cudaEventRecord(hp.kdone[k], st);
         if (e != cudaSuccess) return cuda_fail(e);
-        e = cudaMemcpyAsync(surfaces + (size_t)c0 * plane, hp.d_S[k], sizeof(float) * plane * nb,
-                            cudaMemcpyDeviceToHost, st);
+        e = cudaMemcpyAsync(static_cast<char*>(surfaces) + (size_t)c0 * plane * out_elem_bytes(h), hp.d_S[k],
+                            out_elem_bytes(h) * plane * nb, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaEventRecord(hp.done[k], st);
         if (e != cudaSuccess) return cuda_fail(e);
     }

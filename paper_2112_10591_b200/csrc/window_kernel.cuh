@@ -26,7 +26,7 @@ constexpr int kWinRowWords = kWinWarps + 2;   // E_df words of one row a CTA nee
 
 struct WinParams {
     const uint32_t* __restrict__ Edf;   // [nb][H][NW+2], word w of row y at 1 + w, zero guards
-    float* __restrict__ S;              // [nb][H][W]
+    void* __restrict__ S;               // [nb][H][W] float32 or uint8 (OutT)
     const float* __restrict__ lut;      // [K_sat + 1], lut[K_sat] = 1.0f
     int W, H, NW;
     int K_sat;                          // <= 1024
@@ -54,17 +54,17 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     return v;
 }
 
-// write-once output: streaming store, predicated off for lanes beyond W
-__device__ __forceinline__ void st_cs_pred(float* ptr, float v, uint32_t pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
-                 ::"l"(ptr), "f"(v), "r"(pred) : "memory");
+// write-once output: streaming (evict-first) stores
+__device__ __forceinline__ void st_cs(float* ptr, float v) { __stcs(ptr, v); }
+__device__ __forceinline__ void st_cs(uint8_t* ptr, float v) {
+    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(ptr), "r"((uint32_t)v) : "memory");
 }
 
-template <int C>
+template <int C, typename OutT>
 struct WinState {
     int H, NWP2, lane;
     uint32_t words_sh;                 // shared address of this strip's words (w-1, w, w+1) of row 0
-    float* op;                         // next pixel to emit (rows are emitted in order)
+    OutT* op;                          // next pixel to emit (rows are emitted in order)
     size_t W;                          // row stride in elements
     uint32_t lut_sh, K_sat, xvalid;
 
@@ -79,7 +79,7 @@ struct WinState {
     }
     __device__ __forceinline__ void emit(uint32_t v) {
         const float f = lds_f32(lut_sh + 4u * min(v, K_sat));
-        if (xvalid) __stcs(op, f);   // write-once output: streaming (evict-first) store
+        if (xvalid) st_cs(op, f);
         op += W;
     }
 
@@ -123,7 +123,7 @@ struct WinState {
     }
 };
 
-template <int C>
+template <int C, typename OutT>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
     static_assert(C >= 2 && C <= 31, "window size (hdist_words reports empty words as 31)");
     extern __shared__ __align__(16) uint32_t wsm[];   // [H + 2][kWinRowWords] E_df words, then the table
@@ -147,13 +147,13 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     const int w = w0 + warp;
     if (w >= p.NW) return;
     const int x = 32 * w + lane;
-    WinState<C> st;
+    WinState<C, OutT> st;
     st.H = H;
     st.NWP2 = NWP2;
     st.lane = lane;
     st.W = (size_t)p.W;
     st.xvalid = x < p.W ? 1u : 0u;
-    st.op = p.S + (size_t)b * H * p.W + (x < p.W ? x : 0);
+    st.op = reinterpret_cast<OutT*>(p.S) + (size_t)b * H * p.W + (x < p.W ? x : 0);
     st.K_sat = (uint32_t)p.K_sat;
     uint32_t lut_sh = (uint32_t)__cvta_generic_to_shared(lut_s);
     asm volatile("" : "+r"(lut_sh));   // keep the shared address in a register

@@ -53,9 +53,14 @@ def test_create_rejects_bad_config_before_touching_cuda(lib):
     from paper_2112_10591_b200._lib import IEDS_EINVAL, IedsConfig
 
     h = ctypes.c_void_p()
-    for cfg in [IedsConfig(0, 10, 1, 4, 1.0, 0, 0, 0), IedsConfig(10, 10, 5, 4, 1.0, 0, 0, 0),
-                IedsConfig(10, 10, 1, 0, 1.0, 0, 0, 0), IedsConfig(10, 10, 1, 4, float("nan"), 0, 0, 0),
-                IedsConfig(10, 10, 1, 4, -2.0, 0, 0, 0), IedsConfig(10, 3000, 1, 4, 1.0, 0, 0, 0), IedsConfig(10, 10, 1, 4, 1.0, 0, 0, 8)]:
+    def cfg_(w=10, h_=10, nd=1, nf=4, a=1.0, flags=0, transfer=0, bound=6.0, fmt=0):
+        return IedsConfig(w, h_, nd, nf, a, 0, 0, flags, transfer, bound, fmt)
+
+    bad = [cfg_(w=0), cfg_(nd=5), cfg_(nf=0), cfg_(a=float("nan")), cfg_(a=-2.0), cfg_(h_=3000),
+           cfg_(flags=8), cfg_(transfer=4), cfg_(transfer=2, bound=0.0), cfg_(fmt=2),
+           cfg_(transfer=1, fmt=1),          # 8-bit coding only for Eq. (1)
+           cfg_(a=50.0, fmt=1)]              # 8-bit saturation beyond the 1024-entry table
+    for cfg in bad:
         assert lib.ieds_create(ctypes.byref(cfg), ctypes.byref(h)) == IEDS_EINVAL
         assert not h.value
     assert lib.ieds_create(None, ctypes.byref(h)) == IEDS_EINVAL

@@ -1,0 +1,83 @@
+"""GPU parity of SURVEY §8 row f1: the ablation transfers of §IV-D (Fig. 4) and the
+8-bit coded surface, against the oracle, on both the default (saturation-aware, when
+the transfer saturates) and the exact-EDT kernel.
+
+Tolerances: 8-bit codes are bit-exact (both sides round the fp64 value); fp32 transfers within
+atol 2e-6 + rtol 2^-23 (one rounding of a value up to ~1.5e3 for Id(d)).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth.events import WORKLOADS, batch_events, pattern_events, random_frame_events
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(xy, off, W, H, n_d, n_f, transfer, out, with_d2, bound=6.0, d_sat=6.0):
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    dev = torch.device("cuda", 0)
+    B = len(off) - 1
+    txy = torch.from_numpy(np.ascontiguousarray(xy).view(np.int32)).to(dev)
+    toff = torch.from_numpy(np.asarray(off, np.int64)).to(dev)
+    d2 = torch.empty((B, H, W), dtype=torch.int32, device=dev) if with_d2 else None
+    with ieds.Builder(W, H, n_d, n_f, d_sat=d_sat, device=0, transfer=transfer, bound=bound, out=out) as bld:
+        S = bld.build_batch(txy, toff, sqdist=d2)
+        bld.sync()
+    return S.cpu().numpy(), (d2.cpu().numpy().view(np.uint32) if with_d2 else None)
+
+
+def _windows():
+    wl = WORKLOADS["C1"]
+    c = wl.scene
+    xy, off = batch_events(c, wl.seed, 3, 3)
+    wins = [xy[off[b]:off[b + 1]] for b in range(3)]
+    wins += [pattern_events(c.width, c.height, "empty"), pattern_events(c.width, c.height, "corners"),
+             random_frame_events(c.width, c.height, 0.003, seed=5)]
+    off = np.zeros(len(wins) + 1, np.int64)
+    off[1:] = np.cumsum([len(w) for w in wins])
+    return np.concatenate(wins).astype(np.uint32), off, c.width, c.height
+
+
+@pytest.mark.parametrize("transfer", ["invexp", "linear", "bounded", "log"])
+def test_transfer_variants_f32(transfer):
+    xy, off, W, H = _windows()
+    a = oracle.alpha_from_dsat(6.0)
+    S_def, _ = _run(xy, off, W, H, 0, 5, transfer, "f32", with_d2=False)
+    S_exact, D2 = _run(xy, off, W, H, 0, 5, transfer, "f32", with_d2=True)
+    for b in range(len(off) - 1):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, 0, 5, a)
+        exp = oracle.transfer(ref["D2"], transfer, alpha=a, bound=6.0)
+        for S in (S_def[b], S_exact[b]):
+            fin = np.isfinite(exp)
+            assert np.array_equal(np.isinf(S), ~fin), (transfer, b)
+            err = np.abs(S[fin].astype(np.float64) - exp[fin])
+            assert np.all(err <= 2e-6 + np.abs(exp[fin]) * 2.0 ** -23), (transfer, b, float(err.max()))
+    assert np.array_equal(S_def, S_exact)   # both kernels give the same fp32 bits
+
+
+def test_surface_u8_bit_exact():
+    xy, off, W, H = _windows()
+    a = oracle.alpha_from_dsat(6.0)
+    Q_def, _ = _run(xy, off, W, H, 1, 4, "invexp", "u8", with_d2=False)
+    Q_exact, _ = _run(xy, off, W, H, 1, 4, "invexp", "u8", with_d2=True)
+    assert Q_def.dtype == np.uint8
+    for b in range(len(off) - 1):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, 1, 4, a)
+        q = oracle.quantize_u8(ref["S"])
+        assert np.array_equal(Q_def[b], q), b
+        assert np.array_equal(Q_exact[b], q), b
+
+
+def test_u8_workload_c3_sampled():
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 40, 4)
+    Q, _ = _run(xy, off, c.width, c.height, wl.n_d, wl.n_f, "invexp", "u8", with_d2=False)
+    for b in range(4):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a)
+        assert np.array_equal(Q[b], oracle.quantize_u8(ref["S"])), b
