@@ -369,6 +369,44 @@ def run_ours(args):
                  "achieved_gbs": xe_bytes / (xe_avg / 1e3) / 1e9, "frac": xe_bytes / (xe_avg / 1e3) / 1e9 / peak,
                  "note": "IEDS_FLAG_EXACT_EDT: D2 exact everywhere (the kernel sqdist requests use)"}
 
+    # row f1: the same workload with the 8-bit coded surface, 1 B/px written
+    f1 = None
+    if not args.no_f1:
+        Q = torch.empty((nwin, H, W), dtype=torch.uint8, device=dev)
+        bq = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local, out="u8")
+        for _ in range(max(1, args.warmup)):
+            bq.build_batch(txy, toff, Q)
+        torch.cuda.synchronize(dev)
+        bq.profile(True)
+        bq.profile_read()
+        ksteps = max(1, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(ksteps):
+            bq.build_batch(txy, toff, Q)
+        q1.record(stream)
+        torch.cuda.synchronize(dev)
+        qp = bq.profile_read()
+        bq.sync()
+        bq.close()
+        tq = torch.tensor([q0.elapsed_time(q1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tq, op=dist.ReduceOp.MAX)
+        qms = float(tq.item()) / ksteps
+        qe_ms, qe_n = qp["edt"]
+        q_bytes = 1.0 * W * H * (nwin / max(1, qe_n // ksteps))
+        q_gbs = q_bytes / (qe_ms / max(1, qe_n) / 1e3) / 1e9
+        path_q = (4.0 * n_ev + 1.0 * W * H * nwin) / (qms / 1e3) / 1e9
+        f1 = {"variant": "8-bit coded surface q = round(255*S) (P:231)", "value": total_windows / (qms / 1e3),
+              "unit": UNIT, "ms_per_step": qms, "steps": ksteps,
+              "window_kernel_gbs": q_gbs, "window_kernel_frac": q_gbs / peak,
+              "path_gbs": path_q, "path_frac": path_q / peak,
+              "note": "algorithmic bytes 4 B/event + 1 B/px; saturation radius C = 8 (q = 255 from D2 >= 46)"}
+        del Q
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -413,6 +451,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "exact_edt_path": exact,
+        "f1_u8_surface": f1,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -431,6 +470,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-EDT comparison run")
+    ap.add_argument("--no-f1", action="store_true", help="skip the 8-bit surface (row f1) run")
     ap.add_argument("--cpu-windows", type=int, default=256,
                     help="oracle windows timed for cpu_baseline (~15 core-seconds at 1280x720)")
     ap.add_argument("--traffic", type=float, default=None,

@@ -15,7 +15,8 @@
 // one packed 3-way min (VIMNMX3.U16x2, two rows per instruction); pixel u-C+1 is final after
 // row u and is emitted with one coalesced 128-byte store per warp.  The loop is unrolled over
 // the 2C slot phases so every slot/distance is a compile-time constant: no stack, no
-// divergence, no shared-memory traffic besides the 4-byte table lookup.
+// divergence, no shared-memory traffic besides the 4-byte table lookup.  (Each update is one
+// fused packed add+min instruction, VIADDMNMX.U16x2, per register and row.)
 #pragma once
 #include <cstdint>
 
@@ -101,7 +102,9 @@ struct WinState {
                 const uint32_t sqb = dsq<C>(2 * j, 1) | (dsq<C>(2 * j + 1, 1) << 16);
                 const int m = (j + S + 1) % C;
                 const uint32_t prev = (j + 1 < C) ? P[m] : 0xFFFFFFFFu;
-                P[m] = __vminu2(prev, __vminu2(sqa + h2a, sqb + h2b));
+                // two fused packed add+min (VIADDMNMX.U16x2 with an immediate): no carries
+                // cross the halves because every sum stays below 2 * 31^2 < 2^16
+                P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sqa)), __vadd2(h2b, sqb));
             }
         } else {
             P[S % C] = 0xFFFFFFFFu;   // the new last register starts empty
