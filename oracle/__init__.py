@@ -51,6 +51,8 @@ def _load():
             lib.oracle_surface.argtypes = [P, i64, f64, P]
             lib.oracle_transfer.argtypes = [P, i64, i32, f64, f64, P]
             lib.oracle_quantize_u8.argtypes = [P, i64, P]
+            lib.oracle_window_offsets.argtypes = [P, i64, i64, P, i64]
+            lib.oracle_window_offsets.restype = i64
             lib.oracle_alpha_from_dsat.argtypes = [f64]
             lib.oracle_alpha_from_dsat.restype = f64
             lib.oracle_build_window.argtypes = [P, i64, i32, i32, i32, i32, f64, P, P, P, P, P]
@@ -114,6 +116,22 @@ def surface(D2, alpha: float) -> np.ndarray:
     out = np.empty(D2.shape, np.float64)
     _load().oracle_surface(_ptr(D2), D2.size, float(alpha), _ptr(out))
     return out
+
+
+def window_offsets(t_us, dt_us: int, max_windows: int = 1 << 24) -> np.ndarray:
+    """CSR offsets of the Delta-T windows of a time-ordered stream (row f2, §III-A)."""
+    t = np.ascontiguousarray(t_us, dtype=np.int64)
+    n = len(t)
+    est = 1 if n == 0 else min(max_windows, (int(t[-1]) - int(t[0])) // max(1, int(dt_us)) + 2) if n else 1
+    out = np.zeros(max(est, 1) + 1, np.int64)
+    k = _load().oracle_window_offsets(_ptr(t), n, int(dt_us), _ptr(out), len(out) - 1)
+    if k == -1:
+        raise ValueError("dt must be > 0")
+    if k == -3:
+        raise ValueError("timestamps not ordered")
+    if k == -4:
+        raise ValueError("too many windows")
+    return out[:k + 1]
 
 
 TRANSFERS = {"invexp": 0, "linear": 1, "bounded": 2, "log": 3}

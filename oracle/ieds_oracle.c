@@ -222,6 +222,31 @@ void oracle_surface(const int64_t *D2, int64_t n, double alpha, double *S)
     }
 }
 
+/* ---- Windowing of the event stream by Delta T (§III-A; row f2) ---------------
+ * Events are time-ordered (t in microseconds).  Window k holds the events with
+ * floor((t - t0) / dt) == k, i.e. t in [t0 + k dt, t0 + (k+1) dt) (half-open), where t0 is the
+ * first event's timestamp (reading R16; empty interior windows are
+ * emitted, trailing empty windows are not).  Writes offsets[0..K] (K = number of windows, i.e.
+ * floor((t_last - t0)/dt) + 1) and returns K, 0 for no events, or ORACLE_EINVAL if dt <= 0,
+ * -3 (ordering error) if t is not non-decreasing, or -4 if more than max_windows windows. */
+int64_t oracle_window_offsets(const int64_t *t, int64_t n, int64_t dt, int64_t *offsets, int64_t max_windows)
+{
+    if (dt <= 0) return ORACLE_EINVAL;
+    if (n == 0) { offsets[0] = 0; return 0; }
+    for (int64_t i = 1; i < n; i++)
+        if (t[i] < t[i - 1]) return -3;
+    const int64_t t0 = t[0];
+    const int64_t K = (t[n - 1] - t0) / dt + 1;
+    if (K > max_windows) return -4;
+    int64_t i = 0;
+    for (int64_t k = 0; k <= K; k++) {
+        /* first event of window k (or n) */
+        while (i < n && (t[i] - t0) / dt < k) i++;
+        offsets[k] = i;
+    }
+    return K;
+}
+
 /* ---- Ablation transfers of §IV-D (Fig. 4) --------------------------
  *   kind 0: Eq. (1) inverse exponential  1 - exp(-d/alpha)           (proposed)
  *   kind 1: linear distance transform    Id(d) = d                   (Ours_DS_L,  P:306)

@@ -313,3 +313,30 @@ def test_quantize_u8_saturation():
     assert list(q) == [0, 254, 255, 255]
     # round half away from zero: 0.5/255 -> 1, just below -> 0
     assert list(oracle.quantize_u8(np.array([0.5 / 255.0, 0.49 / 255.0, 1.0]))) == [1, 0, 255]
+
+
+# ---------------------------------------------------------------- row f2: Delta-T windowing
+
+def test_window_offsets_spec_examples():
+    # events at t=0 and t=dt -> two windows ("boundary falls in next window")
+    assert list(oracle.window_offsets([0, 15000], 15000)) == [0, 1, 2]
+    # window count = floor((t_last - t0)/dt) + 1; empty interior windows emitted
+    t = [1000, 1001, 31000 + 1000, 31001 + 1000]
+    off = oracle.window_offsets(t, 15000)
+    assert list(off) == [0, 2, 2, 4] and len(off) - 1 == (t[-1] - t[0]) // 15000 + 1
+    assert list(oracle.window_offsets([], 15000)) == [0]
+    with pytest.raises(ValueError):
+        oracle.window_offsets([5, 4], 10)
+    with pytest.raises(ValueError):
+        oracle.window_offsets([5, 6], 0)
+
+
+def test_window_offsets_match_floor_rule():
+    rng = np.random.default_rng(3)
+    t = np.sort(rng.integers(10_000, 200_000, 5000))
+    dt = 7000
+    off = oracle.window_offsets(t, dt)
+    k_of = (t - t[0]) // dt                          # floor((t - t0)/dt)
+    for k in range(len(off) - 1):
+        assert np.all(k_of[off[k]:off[k + 1]] == k)
+    assert off[-1] == len(t)
