@@ -407,6 +407,35 @@ def run_ours(args):
               "note": "algorithmic bytes 4 B/event + 1 B/px; saturation radius C = 8 (q = 255 from D2 >= 46)"}
         del Q
 
+    # row f2: single-window latency (the paper's real-time mode): one window's
+    # events -> surface, (a) events resident on the device, (b) through the host-buffer API
+    lat = None
+    if not args.no_latency:
+        bl = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local, chunk_windows=1)
+        S1 = torch.empty((1, H, W), dtype=torch.float32, device=dev)
+        hS1 = torch.empty((1, H, W), dtype=torch.float32).pin_memory().numpy()
+        dev_ms, host_ms = [], []
+        for i in range(60):
+            o = off[i:i + 2].copy()
+            xs = xy[o[0]:o[1]]
+            ta = toff[i:i + 2]
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            bl.build_batch(txy, ta, S1)
+            torch.cuda.synchronize(dev)
+            dev_ms.append(1e3 * (time.perf_counter() - t0))
+            t0 = time.perf_counter()
+            bl.build_batch_host(xs, o - o[0], hS1)
+            host_ms.append(1e3 * (time.perf_counter() - t0))
+        bl.close()
+        dev_ms, host_ms = np.array(dev_ms[10:]), np.array(host_ms[10:])
+        lat = {"device_ms_p50": float(np.median(dev_ms)), "device_ms_p99": float(np.percentile(dev_ms, 99)),
+               "host_e2e_ms_p50": float(np.median(host_ms)), "host_e2e_ms_p99": float(np.percentile(host_ms, 99)),
+               "windows": len(dev_ms),
+               "note": "one 1280x720 window per call, wall clock incl. launch + sync; host_e2e adds the H2D of "
+                       "its events and the D2H of its 3.7 MB surface (paper: 16.88 ms per window for the "
+                       "whole pipeline incl. flow on an RTX 5000, P:555)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -452,6 +481,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "exact_edt_path": exact,
         "f1_u8_surface": f1,
+        "f2_latency": lat,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -471,6 +501,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-EDT comparison run")
     ap.add_argument("--no-f1", action="store_true", help="skip the 8-bit surface (row f1) run")
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--cpu-windows", type=int, default=256,
                     help="oracle windows timed for cpu_baseline (~15 core-seconds at 1280x720)")
     ap.add_argument("--traffic", type=float, default=None,

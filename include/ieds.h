@@ -120,6 +120,16 @@ int ieds_build_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *w
 int ieds_build_batch_host(ieds_handle *h, const uint32_t *events_xy,
                           const int64_t *window_offsets, int32_t num_windows, void *surfaces);
 
+/* Row f2 -- windowing of a time-ordered stream (§III-A).  DEVICE pointers.
+ * t_us [n] int64 timestamps (non-decreasing; otherwise IEDS_EORDER is latched for ieds_sync),
+ * t0_us = the first timestamp, dt_us > 0 the window length Delta T, num_windows =
+ * floor((t_last - t0)/dt) + 1.  Writes window_offsets [num_windows + 1]: window k is
+ * events [offsets[k], offsets[k+1]) = the events with floor((t - t0)/dt) == k (half-open
+ * windows; empty interior windows are emitted).  The events array in the same order is then
+ * the events_xy input of ieds_build_batch.  Enqueued on `stream`; no host sync. */
+int ieds_window_offsets(ieds_handle *h, const int64_t *t_us, int64_t n, int64_t t0_us, int64_t dt_us,
+                        int32_t num_windows, int64_t *window_offsets, void *stream);
+
 /* Wait for `stream`, then return (and clear) the latched device error, or IEDS_OK. */
 int ieds_sync(ieds_handle *h, void *stream);
 

@@ -161,6 +161,26 @@ class Builder:
                                       _ptr(sqdist), self._stream(stream)), "ieds_build_batch")
         return out
 
+    def window_offsets(self, t_us, dt_us: int, stream=None):
+        """Row f2: CSR offsets [K+1] (int64, on the device) of the Delta-T windows of a
+        time-ordered int64 timestamp tensor t_us (window k = floor((t - t0)/dt) == k, t0 = t[0]).
+        Reads the first and last timestamps to size the output; ordering errors are latched
+        and raised by sync()."""
+        import torch
+
+        self._check_dev(t_us, "t_us", (torch.int64,))
+        n = t_us.numel()
+        if dt_us <= 0:
+            raise ValueError("dt_us must be > 0")
+        if n == 0:
+            return torch.zeros(1, dtype=torch.int64, device=self.device)
+        t0, t1 = (int(v) for v in t_us[[0, n - 1]].tolist())
+        K = max(0, (t1 - t0) // int(dt_us) + 1) if t1 >= t0 else 1
+        off = torch.empty(K + 1, dtype=torch.int64, device=self.device)
+        check(load().ieds_window_offsets(self._h, _ptr(t_us), n, t0, int(dt_us), K, _ptr(off),
+                                         self._stream(stream)), "ieds_window_offsets")
+        return off
+
     def sync(self, stream=None):
         """Wait for the stream; raise IedsRangeError / IedsOrderError on latched data errors."""
         check(load().ieds_sync(self._h, self._stream(stream)), "ieds_sync")

@@ -17,6 +17,7 @@
 #include "frame_kernel.cuh"
 #include "edt_kernel.cuh"
 #include "window_kernel.cuh"
+#include "windowing_kernel.cuh"
 
 #ifndef IEDS_VERSION_STR
 #define IEDS_VERSION_STR "ieds-b200 0.1 (sm_100a)"
@@ -501,6 +502,18 @@ int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* w
         if (rc != IEDS_OK) return rc;
     }
     return IEDS_OK;
+}
+
+int ieds_window_offsets(ieds_handle* h, const int64_t* t_us, int64_t n, int64_t t0_us, int64_t dt_us,
+                        int32_t num_windows, int64_t* window_offsets, void* stream) {
+    if (!h || n < 0 || dt_us <= 0 || num_windows < 0 || !window_offsets || (n > 0 && !t_us)) return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t work = std::max<int64_t>(num_windows + 1, n);
+    const int blocks = (int)std::min<int64_t>(4 * 148, std::max<int64_t>(1, (work + 255) / 256));
+    ieds::window_offsets_kernel<<<blocks, 256, 0, st>>>(t_us, n, t0_us, dt_us, num_windows, window_offsets, h->err);
+    return cudaGetLastError() == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
 }
 
 int ieds_sync(ieds_handle* h, void* stream) {

@@ -1,0 +1,36 @@
+// windowing_kernel.cuh -- row f2: CSR window offsets of a time-ordered event stream.
+//
+// §III-A: events are accumulated over windows of length Delta T.  Window k holds
+// the events with floor((t - t0) / dt) == k, t in [t0 + k dt, t0 + (k+1) dt) -- reading R16
+// (t0 = first timestamp; interior empty windows are emitted).  offsets[k] is the first event
+// with t >= t0 + k dt, found by binary search (one thread per window boundary); a second grid
+// stride checks that the timestamps are non-decreasing and latches kErrOrder otherwise.
+#pragma once
+#include <cstdint>
+
+namespace ieds {
+
+__global__ void window_offsets_kernel(const int64_t* __restrict__ t, int64_t n, int64_t t0, int64_t dt,
+                                      int64_t K, int64_t* __restrict__ offsets, int* __restrict__ err) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = tid; k <= K; k += nthr) {
+        int64_t lo = 0, hi = n;
+        if (k == K) {
+            lo = n;
+        } else {
+            const int64_t key = t0 + k * dt;
+            while (lo < hi) {   // first index with t >= key
+                const int64_t mid = lo + ((hi - lo) >> 1);
+                if (__ldg(t + mid) < key) lo = mid + 1;
+                else hi = mid;
+            }
+        }
+        offsets[k] = lo;
+    }
+    bool bad = false;
+    for (int64_t i = tid + 1; i < n; i += nthr) bad |= __ldg(t + i) < __ldg(t + i - 1);
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrOrder);
+}
+
+}  // namespace ieds

@@ -81,3 +81,48 @@ def test_u8_workload_c3_sampled():
     for b in range(4):
         ref = oracle.build_window(xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a)
         assert np.array_equal(Q[b], oracle.quantize_u8(ref["S"])), b
+
+
+# ----------------------------------------------------------------------------- row f2
+
+def _stream(n_win=6, dt=15000):
+    """A time-ordered Gen4-like stream: the generator's windows k laid end to end in time,
+    with one empty interior window (events of window 3 dropped)."""
+    from synth.events import GEN4, window_events
+
+    xs, ts = [], []
+    for k in range(n_win):
+        xy, t, _ = window_events(GEN4, 3, k, with_tp=True)
+        if k == 3:
+            continue
+        xs.append(xy)
+        ts.append(t)
+    return np.concatenate(xs), np.concatenate(ts), dt
+
+
+def test_window_offsets_match_oracle_and_build():
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    xy, t, dt = _stream()
+    ref_off = oracle.window_offsets(t, dt)
+    dev = torch.device("cuda", 0)
+    with ieds.Builder(1280, 720, 2, 3, d_sat=6.0, device=0) as bld:
+        off = bld.window_offsets(torch.from_numpy(t).to(dev), dt)
+        S = bld.build_batch(torch.from_numpy(xy.view(np.int32)).to(dev), off)
+        bld.sync()
+        got = off.cpu().numpy()
+        assert np.array_equal(got, ref_off)
+        assert got[4] == got[3]                       # the empty interior window is emitted
+        a = oracle.alpha_from_dsat(6.0)
+        S = S.cpu().numpy()
+        for k in (0, 3, 5):
+            ref = oracle.build_window(xy[ref_off[k]:ref_off[k + 1]], 1280, 720, 2, 3, a)
+            assert np.abs(S[k] - ref["S"]).max() <= 2e-6
+        # unordered timestamps are latched as an ordering error
+        bad = t.copy()
+        bad[10], bad[11] = bad[11] + 1, bad[10]
+        bld.window_offsets(torch.from_numpy(bad).to(dev), dt)
+        with pytest.raises(ieds.IedsOrderError):
+            bld.sync()
