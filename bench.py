@@ -257,7 +257,7 @@ def run_ours(args):
     txy = torch.from_numpy(xy.view(np.int32)).to(dev)
     toff = torch.from_numpy(off).to(dev)
     S = torch.empty((nwin, H, W), dtype=torch.float32, device=dev)
-    bld = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
+    bld = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local, chunk_windows=args.chunk)
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
@@ -502,6 +502,7 @@ def main():
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-EDT comparison run")
     ap.add_argument("--no-f1", action="store_true", help="skip the 8-bit surface (row f1) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
+    ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")
     ap.add_argument("--cpu-windows", type=int, default=256,
                     help="oracle windows timed for cpu_baseline (~15 core-seconds at 1280x720)")
     ap.add_argument("--traffic", type=float, default=None,

@@ -71,7 +71,8 @@ typedef struct {
     int32_t n_f;            /* 1 .. 5, filling threshold N_f (5 disables)         */
     double alpha;           /* > 0 and finite, spreading parameter of Eq. (1), pixels    */
     int32_t chunk_windows;  /* windows processed per launch pair (sizes the scratch);    */
-                            /* batches of any size are processed chunk by chunk. 0 = 128 */
+                            /* batches of any size are processed chunk by chunk.         */
+                            /* 0 = 8 x SM count; the host path pipelines 2 x SM count    */
     int32_t device;         /* CUDA device ordinal; -1 = current device                 */
     int32_t flags;          /* IEDS_FLAG_* bits                                          */
     int32_t transfer;       /* IEDS_TRANSFER_*; 0 = Eq. (1)                             */

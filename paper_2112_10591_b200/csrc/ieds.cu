@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kFrameThreads = 1024;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
-constexpr int kLutMax = 1024;
+constexpr int kLutMax = ieds::kWinLutMax;
 constexpr int kSegTarget = 80;     // columns per EDT segment (warp)
 
 struct HostPath {
@@ -54,13 +54,15 @@ struct ieds_handle {
     ieds_config cfg;
     int dev;
     int NW, NWP, NR, NS, SEGW;
-    int chunk;
+    int chunk;        // windows per launch pair of the device path (scratch capacity)
+    int host_chunk;   // windows per pipelined copy/compute step of the host path (<= chunk)
     size_t smem_frame, smem_edt, smem_edt_d2;
     int c_sat;                 // ceil(sqrt(K_sat)): rows/columns a near site can be away
     int c_win;                 // window size of the branch-free kernel (>= c_sat)
     bool streaming;            // saturation-aware window kernel usable (K_sat <= 1024)
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
+    uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
     unsigned long long* colmask = nullptr;
     int* err = nullptr;
     int* h_err = nullptr;   // pinned
@@ -180,7 +182,7 @@ int window_size_for(int c) {
     return 0;
 }
 
-size_t window_smem_bytes(int H) { return 4ull * ((H + 2) * ieds::kWinRowWords + 1028); }
+size_t window_smem_bytes(int H) { return 4ull * ieds::window_staged_rows(H) * ieds::kWinRowWords; }
 
 template <int C>
 void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, bool u8) {
@@ -268,6 +270,8 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
         wp.H = h->cfg.height;
         wp.NW = h->NW;
         wp.K_sat = h->K_sat;
+        wp.dummy = h->dummy;
+        wp.one = 1u;
         dim3 wgrid((h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps, nb);
         prof_pair(h, 1, &pa, &pb);
         if (pa) cudaEventRecord(pa, st);
@@ -397,7 +401,12 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
 
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    h->chunk = cfg->chunk_windows > 0 ? cfg->chunk_windows : 2 * nsm;
+    // Default: 8 waves of windows per launch pair (~143 MB of scratch at 1280x720), so a
+    // 1000-window batch is one frame launch + one window launch with a single partial tail
+    // wave instead of four launch pairs whose last one runs a mostly idle wave.  The host
+    // path pipelines copies against kernels at a finer 2-wave grain.
+    h->chunk = cfg->chunk_windows > 0 ? cfg->chunk_windows : 8 * nsm;
+    h->host_chunk = std::min(h->chunk, 2 * nsm);
 
     cudaError_t e;
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
@@ -407,6 +416,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
+    if (e == cudaSuccess) e = cudaMalloc(&h->dummy, sizeof(uint32_t) * 32 * (size_t)h->chunk);
     if (e == cudaSuccess) e = cudaMalloc(&h->colmask, sizeof(unsigned long long) * (size_t)h->chunk * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(int));
@@ -437,6 +447,7 @@ void ieds_destroy(ieds_handle* h) {
     for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
     cudaFree(h->T);
     cudaFree(h->Edfs);
+    cudaFree(h->dummy);
     cudaFree(h->colmask);
     cudaFree(h->err);
     cudaFree(h->lut);
@@ -543,7 +554,7 @@ int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64
     HostPath& hp = h->hp;
     cudaError_t e = cudaSuccess;
     const size_t plane = (size_t)h->cfg.width * h->cfg.height;
-    const int chunk = h->chunk;
+    const int chunk = h->host_chunk;
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         if (!hp.st[i]) e = cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking);
         if (e == cudaSuccess && !hp.done[i]) e = cudaEventCreateWithFlags(&hp.done[i], cudaEventDisableTiming);

@@ -10,78 +10,85 @@
 // candidate is a true squared distance or >= C^2 >= K_sat, so a computed value >= K_sat can
 // only occur when D2 >= K_sat: the fp32 surface is the exact-EDT surface, bit for bit.
 //
-// Each lane keeps the 2C pixels y in [u-C+1, u+C] of its column as 16-bit partial minima,
-// two per register (slot y mod 2C).  Row u's site updates all of them with one packed add and
-// one packed 3-way min (VIMNMX3.U16x2, two rows per instruction); pixel u-C+1 is final after
-// row u and is emitted with one coalesced 128-byte store per warp.  The loop is unrolled over
-// the 2C slot phases so every slot/distance is a compile-time constant: no stack, no
-// divergence, no shared-memory traffic besides the 4-byte table lookup.  (Each update is one
-// fused packed add+min instruction, VIADDMNMX.U16x2, per register and row.)
+// Each lane keeps the 2C pixels y in [u-C+1, u+C] of its column as 16-bit partial minima of
+// 4*D2, two per register (slot y mod 2C).  Row u's site updates all of them with one fused
+// packed add+min (VIADDMNMX.U16x2 with an immediate) per register and row; pixel u-C+1 is
+// final after row u and is emitted with one coalesced 128-byte store per warp.  The loop is
+// unrolled over the C register phases of one rotation so every slot/distance is a
+// compile-time constant: no stack, no divergence.  The rotations in the middle of the frame
+// (all emitted rows inside the frame) run without any range check; only the first and the
+// last rotation carry them.  Instruction budget per row pair (2 pixels), see DESIGN.md §6:
+//   h of 2 rows   2 x (3 LDS + 2 SHF + BREV + LOP3 + FLO.SH) + 2 x 2 IMAD (packed h^2)
+//   warp vote     2 ISETP + VOTE + BRA (skip the update when no lane has a site < C away)
+//   update        2C VIADDMNMX.U16x2
+//   emit          1 packed clamp + 2 extracts + 2 LDS (table) + 2 STG + 2 IMAD.WIDE (pointer)
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 namespace ieds {
 
-constexpr int kWinWarps = 8;                  // warps (strips) per CTA
-constexpr int kWinRowWords = kWinWarps + 2;   // E_df words of one row a CTA needs (strips +- 1)
+constexpr int kWinWarps = 8;                      // warps (strips) per CTA
+constexpr int kWinRowWords = kWinWarps + 2;       // E_df words of one row a CTA needs (strips +- 1)
+constexpr int kWinRowBytes = 4 * kWinRowWords;
+constexpr int kWinMaxC = 31;
+constexpr int kWinLutMax = 1024;                  // K_sat bound of the window path
 
 struct WinParams {
     const uint32_t* __restrict__ Edf;   // [nb][H][NW+2], word w of row y at 1 + w, zero guards
     void* __restrict__ S;               // [nb][H][W] float32 or uint8 (OutT)
-    const float* __restrict__ lut;      // [K_sat + 1], lut[K_sat] = 1.0f
+    const float* __restrict__ lut;      // [K_sat + 1], lut[K_sat] = the saturated value
+    uint32_t* __restrict__ dummy;       // [nb][32] sink for the lanes of a ragged strip (x >= W)
     int W, H, NW;
-    int K_sat;                          // <= 1024
+    int K_sat;                          // <= kWinLutMax
+    uint32_t one;                       // 1 (a runtime multiplier keeps the pointer step an IMAD.WIDE)
 };
 
-// horizontal distance of lane j of a strip to the nearest set bit of words (tl, t, tr)
-// (>= 32 when none within 31 columns)
-__device__ __forceinline__ int hdist_words(uint32_t tl, uint32_t t, uint32_t tr, int j) {
-    const uint32_t left = __funnelshift_rc(tl, t, j + 1);   // columns x-31..x, x in the MSB
-    const uint32_t right = __funnelshift_r(t, tr, j);       // columns x..x+31, x in the LSB
-    // trailing zeros of `right`; an empty word reads as 31, which is >= C for every C <= 31
-    return min(__clz(left), __ffs(right | 0x80000000u) - 1);
-}
+// rows of dynamic shared memory a CTA stages: H rows plus zero rows for the reads past H
+__host__ __device__ constexpr int window_staged_rows(int H) { return H + kWinMaxC + 1; }
 
-// squared distance from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
+// squared distance x4 from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
 template <int C>
-__device__ __forceinline__ constexpr uint32_t dsq(int j, int row_off) {
+__device__ __forceinline__ constexpr uint32_t dsq4(int j, int row_off) {
     const int d = j - (C - 1) - row_off;
-    return (uint32_t)(d * d);
+    return (uint32_t)(4 * d * d);
 }
 
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
+__device__ __forceinline__ uint32_t clz_shiftamt(uint32_t x) {   // FLO.U32.SH; x != 0
+    uint32_t r;
+    asm("bfind.shiftamt.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
 }
 
-// write-once output: streaming (evict-first) stores
-__device__ __forceinline__ void st_cs(float* ptr, float v) { __stcs(ptr, v); }
-__device__ __forceinline__ void st_cs(uint8_t* ptr, float v) {
-    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(ptr), "r"((uint32_t)v) : "memory");
+// write-once output: streaming (evict-first) stores of the table's raw 32-bit pattern
+__device__ __forceinline__ void st_cs_bits(float*, uint64_t addr, uint32_t bits) {
+    asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(addr), "r"(bits) : "memory");
+}
+__device__ __forceinline__ void st_cs_bits(uint8_t*, uint64_t addr, uint32_t bits) {
+    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(addr), "r"(bits) : "memory");
 }
 
 template <int C, typename OutT>
 struct WinState {
-    int H, NWP2, lane;
-    uint32_t words_sh;                 // shared address of this strip's words (w-1, w, w+1) of row 0
-    OutT* op;                          // next pixel to emit (rows are emitted in order)
-    size_t W;                          // row stride in elements
-    uint32_t lut_sh, K_sat, xvalid;
+    int H, lane;
+    uint64_t op;                       // byte address of the next pixel to emit (rows in order)
+    uint32_t wb, one;                  // row stride in bytes (0 for lanes beyond W), 1
+    uint32_t ksat4x2;                  // 4*K_sat in both halves: the clamp of the table index
+    const uint32_t* lut;               // shared table, raw output bit patterns
 
-    // h of row u for this lane: 3 broadcast shared loads (words w-1, w, w+1 of the row)
-    __device__ __forceinline__ uint32_t h_of(int u) const {
-        const uint32_t a = words_sh + (uint32_t)min(u, H) * (4u * kWinRowWords);
-        uint32_t tl, t, tr;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tl) : "r"(a));
-        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(t) : "r"(a));
-        asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(tr) : "r"(a));
-        return (uint32_t)hdist_words(tl, t, tr, lane);   // <= 31; >= C contributes >= C^2
+    // h of the row at `rp` (this strip's words w-1, w, w+1), clamped to <= 31:
+    // clz of (columns x-31..x with x at the MSB) | bitreverse(columns x..x+31) -- the leading
+    // zero count of an OR is the min of the two one-sided distances; bit 0 bounds it by 31.
+    __device__ __forceinline__ uint32_t h_of(const uint32_t* rp) const {
+        const uint32_t tl = rp[0], t = rp[1], tr = rp[2];
+        const uint32_t left = __funnelshift_rc(tl, t, lane + 1);
+        const uint32_t right = __funnelshift_r(t, tr, lane);
+        return clz_shiftamt(left | __brev(right) | 1u);
     }
-    __device__ __forceinline__ void emit(uint32_t v) {
-        const float f = lds_f32(lut_sh + 4u * min(v, K_sat));
-        if (xvalid) st_cs(op, f);
-        op += W;
+    __device__ __forceinline__ void emit(uint32_t idx4) {
+        const uint32_t bits = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(lut) + idx4);
+        st_cs_bits(static_cast<OutT*>(nullptr), op, bits);
+        asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(op) : "r"(wb), "r"(one));
     }
 
     // Rotating window: before a pair step of phase S, logical register j (pixels y0+2j,
@@ -89,38 +96,44 @@ struct WinState {
     // u, u+1 and shifts the window by one register, in place: logical j of the new window is
     // old logical j+1 min the two parabolas, and the freed register P[S % C] becomes the new
     // last register.  Then pixels y0, y0+1 are final -- a site C or more rows away cannot
-    // bring a value below C^2 >= K_sat -- and are emitted.  Unrolled over S = 0..C-1 (one
-    // rotation) every register index is static and a skipped row pair costs one reset.
-    template <int S>
-    __device__ __forceinline__ void step(int u, uint32_t (&P)[C]) {
-        const uint32_t ha = h_of(u), hb = h_of(u + 1);   // rows >= H are zero words: no site
-        if (__any_sync(0xFFFFFFFFu, (ha < (uint32_t)C) | (hb < (uint32_t)C))) {
-            const uint32_t h2a = ha * ha * 0x10001u, h2b = hb * hb * 0x10001u;
+    // bring a value below C^2 >= K_sat -- and are emitted.  `rows` points at row u0 of the
+    // rotation, so both row reads use immediate offsets.
+    template <int S, bool CHECK>
+    __device__ __forceinline__ void step(const uint32_t* rows, int u0, uint32_t (&P)[C]) {
+        const uint32_t ha = h_of(rows + (2 * S) * kWinRowWords);
+        const uint32_t hb = h_of(rows + (2 * S + 1) * kWinRowWords);   // rows >= H are zero words
+        if (__any_sync(0xFFFFFFFFu, min(ha, hb) < (uint32_t)C)) {
+            const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
-                const uint32_t sqa = dsq<C>(2 * j, 0) | (dsq<C>(2 * j + 1, 0) << 16);
-                const uint32_t sqb = dsq<C>(2 * j, 1) | (dsq<C>(2 * j + 1, 1) << 16);
+                const uint32_t sqa = dsq4<C>(2 * j, 0) | (dsq4<C>(2 * j + 1, 0) << 16);
+                const uint32_t sqb = dsq4<C>(2 * j, 1) | (dsq4<C>(2 * j + 1, 1) << 16);
                 const int m = (j + S + 1) % C;
                 const uint32_t prev = (j + 1 < C) ? P[m] : 0xFFFFFFFFu;
-                // two fused packed add+min (VIADDMNMX.U16x2 with an immediate): no carries
-                // cross the halves because every sum stays below 2 * 31^2 < 2^16
+                // two fused packed add+min: no carries cross the halves because every sum
+                // stays below 4 * (31^2 + 31^2) < 2^16
                 P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sqa)), __vadd2(h2b, sqb));
             }
         } else {
             P[S % C] = 0xFFFFFFFFu;   // the new last register starts empty
         }
-        const int y0 = u - (C - 1);
-        const uint32_t v = P[(S + 1) % C];
-        if (y0 >= 0 && y0 < H) emit(v & 0xFFFFu);
-        if (y0 + 1 >= 0 && y0 + 1 < H) emit(v >> 16);
+        const uint32_t v = __vminu2(P[(S + 1) % C], ksat4x2);
+        if constexpr (CHECK) {
+            const int y0 = u0 + 2 * S - (C - 1);
+            if (y0 >= 0 && y0 < H) emit(v & 0xFFFFu);
+            if (y0 + 1 >= 0 && y0 + 1 < H) emit(v >> 16);
+        } else {
+            emit(v & 0xFFFFu);
+            emit(v >> 16);
+        }
     }
 
-    template <int S>
-    __device__ __forceinline__ void block(int u0, int total, uint32_t (&P)[C]) {
+    template <int S, bool CHECK>
+    __device__ __forceinline__ void block(const uint32_t* rows, int u0, int total, uint32_t (&P)[C]) {
         if constexpr (S < C) {
-            if (u0 + 2 * S < total) {
-                step<S>(u0 + 2 * S, P);
-                block<S + 1>(u0, total, P);
+            if (!CHECK || u0 + 2 * S < total) {
+                step<S, CHECK>(rows, u0, P);
+                block<S + 1, CHECK>(rows, u0, total, P);
             }
         }
     }
@@ -128,23 +141,26 @@ struct WinState {
 
 template <int C, typename OutT>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
-    static_assert(C >= 2 && C <= 31, "window size (hdist_words reports empty words as 31)");
-    extern __shared__ __align__(16) uint32_t wsm[];   // [H + 2][kWinRowWords] E_df words, then the table
+    static_assert(C >= 2 && C <= kWinMaxC, "window size (h is clamped to 31)");
+    __shared__ uint32_t lut_s[kWinLutMax + 1];           // table, raw output bit patterns
+    extern __shared__ __align__(16) uint32_t wsm[];      // [H + kWinMaxC + 1][kWinRowWords] E_df words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
     const int NWP2 = p.NW + 2;
     // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
-    // plus two zero rows past the end for the row pair straddling H
+    // plus zero rows past the end for the reads of the last rotation
     {
         const uint32_t* src = p.Edf + (size_t)b * H * NWP2 + w0;
-        const int n = (H + 2) * kWinRowWords;
+        const int n = window_staged_rows(H) * kWinRowWords;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const int y = i / kWinRowWords, c = i - y * kWinRowWords;
             wsm[i] = (y < H && w0 + c < NWP2) ? __ldg(src + (size_t)y * NWP2 + c) : 0u;
         }
     }
-    float* lut_s = reinterpret_cast<float*>(wsm + (H + 2) * kWinRowWords);
-    for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) lut_s[i] = p.lut[i];
+    for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) {
+        const float f = p.lut[i];
+        lut_s[i] = std::is_same<OutT, uint8_t>::value ? (uint32_t)f : __float_as_uint(f);
+    }
     __syncthreads();
 
     const int w = w0 + warp;
@@ -152,23 +168,30 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     const int x = 32 * w + lane;
     WinState<C, OutT> st;
     st.H = H;
-    st.NWP2 = NWP2;
     st.lane = lane;
-    st.W = (size_t)p.W;
-    st.xvalid = x < p.W ? 1u : 0u;
-    st.op = reinterpret_cast<OutT*>(p.S) + (size_t)b * H * p.W + (x < p.W ? x : 0);
-    st.K_sat = (uint32_t)p.K_sat;
-    uint32_t lut_sh = (uint32_t)__cvta_generic_to_shared(lut_s);
-    asm volatile("" : "+r"(lut_sh));   // keep the shared address in a register
-    st.lut_sh = lut_sh;
-    st.words_sh = (uint32_t)__cvta_generic_to_shared(wsm + warp);
+    st.one = p.one;
+    st.ksat4x2 = (4u * (uint32_t)p.K_sat) * 0x10001u;
+    st.lut = lut_s;
+    if (x < p.W) {
+        st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.S) + ((size_t)b * H * p.W + x));
+        st.wb = (uint32_t)(p.W * sizeof(OutT));
+    } else {   // lanes of a ragged last strip write to a private sink, stride 0
+        st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.dummy + 32 * (size_t)b) + lane);
+        st.wb = 0;
+    }
+    const uint32_t* rows = wsm + warp;   // this strip's words w-1, w, w+1 of row 0
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
     uint32_t P[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) P[k] = 0xFFFFFFFFu;
     const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
-    for (int u = 0; u < total; u += 2 * C) st.template block<0>(u, total, P);
+    // rotation 0 emits rows y0 < 0 (skipped); a rotation u0 >= 2C with u0 + C < H emits only
+    // rows inside the frame and reads only staged rows: no checks there
+    st.template block<0, true>(rows, 0, total, P);
+    int u0 = 2 * C;
+    for (; u0 + C < H; u0 += 2 * C) st.template block<0, false>(rows + u0 * kWinRowWords, u0, total, P);
+    for (; u0 < total; u0 += 2 * C) st.template block<0, true>(rows + u0 * kWinRowWords, u0, total, P);
 }
 
 }  // namespace ieds
