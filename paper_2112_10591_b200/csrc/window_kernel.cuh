@@ -21,7 +21,7 @@
 //   h of 2 rows   2 x (3 LDS + 2 SHF + BREV + LOP3 + FLO.SH) + 2 x 2 IMAD (packed h^2)
 //   warp vote     2 ISETP + VOTE + BRA (skip the update when no lane has a site < C away)
 //   update        2C VIADDMNMX.U16x2
-//   emit          1 packed clamp + 2 extracts + 2 LDS (table) + 2 STG + 2 IMAD.WIDE (pointer)
+//   emit          2 IMAD extracts + 2 LDS (table) + 2 STG + 2 32-bit pointer adds
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -41,7 +41,7 @@ struct WinParams {
     uint32_t* __restrict__ dummy;       // [nb][32] sink for the lanes of a ragged strip (x >= W)
     int W, H, NW;
     int K_sat;                          // <= kWinLutMax
-    uint32_t one;                       // 1 (a runtime multiplier keeps the pointer step an IMAD.WIDE)
+    uint32_t one;                       // 1 (runtime, so 0x10000 = one << 16 stays an IMAD operand)
 };
 
 // rows of dynamic shared memory a CTA stages: H rows plus zero rows for the reads past H
@@ -72,8 +72,9 @@ template <int C, typename OutT>
 struct WinState {
     int H, lane;
     uint64_t op;                       // byte address of the next pixel to emit (rows in order)
-    uint32_t wb, one;                  // row stride in bytes (0 for lanes beyond W), 1
-    uint32_t ksat4x2;                  // 4*K_sat in both halves: the clamp of the table index
+    uint32_t wb;                       // row stride in bytes (0 for lanes beyond W)
+    uint32_t k65536;                   // 0x10000 (runtime: the half extracts stay IMADs)
+    uint32_t ksat4x2;                  // 4*K_sat in both halves: the start value of every slot
     const uint32_t* lut;               // shared table, raw output bit patterns
 
     // h of the row at `rp` (this strip's words w-1, w, w+1), clamped to <= 31:
@@ -85,10 +86,18 @@ struct WinState {
         const uint32_t right = __funnelshift_r(t, tr, lane);
         return clz_shiftamt(left | __brev(right) | 1u);
     }
+    // store table[idx4 / 4] at op and step op one row down; FAST: the rows left in this
+    // window do not cross a 4 GB boundary, so only the low address word moves
+    template <bool FAST>
     __device__ __forceinline__ void emit(uint32_t idx4) {
         const uint32_t bits = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(lut) + idx4);
         st_cs_bits(static_cast<OutT*>(nullptr), op, bits);
-        asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(op) : "r"(wb), "r"(one));
+        if constexpr (FAST) {
+            asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %0;\n\tadd.u32 lo, lo, %1;\n\t"
+                "mov.b64 %0, {lo, hi};\n\t}" : "+l"(op) : "r"(wb));
+        } else {
+            op += wb;
+        }
     }
 
     // Rotating window: before a pair step of phase S, logical register j (pixels y0+2j,
@@ -96,9 +105,10 @@ struct WinState {
     // u, u+1 and shifts the window by one register, in place: logical j of the new window is
     // old logical j+1 min the two parabolas, and the freed register P[S % C] becomes the new
     // last register.  Then pixels y0, y0+1 are final -- a site C or more rows away cannot
-    // bring a value below C^2 >= K_sat -- and are emitted.  `rows` points at row u0 of the
-    // rotation, so both row reads use immediate offsets.
-    template <int S, bool CHECK>
+    // bring a value below C^2 >= K_sat -- and are emitted.  Slots start at 4*K_sat and only
+    // decrease, so every emitted value is a valid table offset.  `rows` points at row u0 of
+    // the rotation, so both row reads use immediate offsets.
+    template <int S, bool FAST>
     __device__ __forceinline__ void step(const uint32_t* rows, int u0, uint32_t (&P)[C]) {
         const uint32_t ha = h_of(rows + (2 * S) * kWinRowWords);
         const uint32_t hb = h_of(rows + (2 * S + 1) * kWinRowWords);   // rows >= H are zero words
@@ -109,31 +119,32 @@ struct WinState {
                 const uint32_t sqa = dsq4<C>(2 * j, 0) | (dsq4<C>(2 * j + 1, 0) << 16);
                 const uint32_t sqb = dsq4<C>(2 * j, 1) | (dsq4<C>(2 * j + 1, 1) << 16);
                 const int m = (j + S + 1) % C;
-                const uint32_t prev = (j + 1 < C) ? P[m] : 0xFFFFFFFFu;
+                const uint32_t prev = (j + 1 < C) ? P[m] : ksat4x2;
                 // two fused packed add+min: no carries cross the halves because every sum
                 // stays below 4 * (31^2 + 31^2) < 2^16
                 P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sqa)), __vadd2(h2b, sqb));
             }
         } else {
-            P[S % C] = 0xFFFFFFFFu;   // the new last register starts empty
+            P[S % C] = ksat4x2;   // the new last register starts empty
         }
-        const uint32_t v = __vminu2(P[(S + 1) % C], ksat4x2);
-        if constexpr (CHECK) {
+        const uint32_t v = P[(S + 1) % C];
+        const uint32_t hi = __umulhi(v, k65536), lo = v - hi * 0x10000u;
+        if constexpr (!FAST) {
             const int y0 = u0 + 2 * S - (C - 1);
-            if (y0 >= 0 && y0 < H) emit(v & 0xFFFFu);
-            if (y0 + 1 >= 0 && y0 + 1 < H) emit(v >> 16);
+            if (y0 >= 0 && y0 < H) emit<false>(lo);
+            if (y0 + 1 >= 0 && y0 + 1 < H) emit<false>(hi);
         } else {
-            emit(v & 0xFFFFu);
-            emit(v >> 16);
+            emit<true>(lo);
+            emit<true>(hi);
         }
     }
 
-    template <int S, bool CHECK>
+    template <int S, bool FAST>
     __device__ __forceinline__ void block(const uint32_t* rows, int u0, int total, uint32_t (&P)[C]) {
         if constexpr (S < C) {
-            if (!CHECK || u0 + 2 * S < total) {
-                step<S, CHECK>(rows, u0, P);
-                block<S + 1, CHECK>(rows, u0, total, P);
+            if (FAST || u0 + 2 * S < total) {
+                step<S, FAST>(rows, u0, P);
+                block<S + 1, FAST>(rows, u0, total, P);
             }
         }
     }
@@ -148,19 +159,30 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
     const int NWP2 = p.NW + 2;
     // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
-    // plus zero rows past the end for the reads of the last rotation
+    // plus zero rows past the end for the reads of the last rotation: asynchronous 4-byte
+    // copies, zero-filled where out of range, all in flight at once
     {
         const uint32_t* src = p.Edf + (size_t)b * H * NWP2 + w0;
-        const int n = window_staged_rows(H) * kWinRowWords;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int y = i / kWinRowWords, c = i - y * kWinRowWords;
-            wsm[i] = (y < H && w0 + c < NWP2) ? __ldg(src + (size_t)y * NWP2 + c) : 0u;
+        constexpr int kRowsPerPass = (kWinWarps * 32) / kWinRowWords;   // 25 rows x 10 words
+        const int c = threadIdx.x % kWinRowWords, y_first = threadIdx.x / kWinRowWords;
+        const bool col_ok = w0 + c < NWP2;
+        const int rows_staged = window_staged_rows(H);
+        if (y_first < kRowsPerPass) {
+            uint32_t dst = (uint32_t)__cvta_generic_to_shared(wsm + y_first * kWinRowWords + c);
+            for (int y = y_first; y < rows_staged; y += kRowsPerPass, dst += 4u * kRowsPerPass * kWinRowWords) {
+                const bool ok = col_ok && y < H;
+                const uint32_t* g = ok ? src + (size_t)y * NWP2 + c : src;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(g), "r"(ok ? 4 : 0)
+                             : "memory");
+            }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) {
         const float f = p.lut[i];
         lut_s[i] = std::is_same<OutT, uint8_t>::value ? (uint32_t)f : __float_as_uint(f);
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     const int w = w0 + warp;
@@ -169,7 +191,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     WinState<C, OutT> st;
     st.H = H;
     st.lane = lane;
-    st.one = p.one;
+    st.k65536 = p.one << 16;
     st.ksat4x2 = (4u * (uint32_t)p.K_sat) * 0x10001u;
     st.lut = lut_s;
     if (x < p.W) {
@@ -179,19 +201,25 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
         st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.dummy + 32 * (size_t)b) + lane);
         st.wb = 0;
     }
+    // the unchecked rotations step only the low address word: every lane's column of this
+    // window must lie inside one 4 GB-aligned range (else all rotations take the checked path)
+    const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(H - 1);
+    const bool fast_ok = __all_sync(0xFFFFFFFFu, (last >> 32) == (st.op >> 32));
     const uint32_t* rows = wsm + warp;   // this strip's words w-1, w, w+1 of row 0
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
     uint32_t P[C];
 #pragma unroll
-    for (int k = 0; k < C; ++k) P[k] = 0xFFFFFFFFu;
+    for (int k = 0; k < C; ++k) P[k] = st.ksat4x2;
     const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
     // rotation 0 emits rows y0 < 0 (skipped); a rotation u0 >= 2C with u0 + C < H emits only
     // rows inside the frame and reads only staged rows: no checks there
-    st.template block<0, true>(rows, 0, total, P);
-    int u0 = 2 * C;
-    for (; u0 + C < H; u0 += 2 * C) st.template block<0, false>(rows + u0 * kWinRowWords, u0, total, P);
-    for (; u0 < total; u0 += 2 * C) st.template block<0, true>(rows + u0 * kWinRowWords, u0, total, P);
+    for (int u0 = 0; u0 < total; u0 += 2 * C) {
+        if (fast_ok && u0 >= 2 * C && u0 + C < H)
+            st.template block<0, true>(rows + u0 * kWinRowWords, u0, total, P);
+        else
+            st.template block<0, false>(rows + u0 * kWinRowWords, u0, total, P);
+    }
 }
 
 }  // namespace ieds
