@@ -182,12 +182,11 @@ int window_size_for(int c) {
     return 0;
 }
 
-size_t window_smem_bytes(int H) { return 4ull * ieds::window_staged_rows(H) * ieds::kWinRowWords; }
 
 template <int C>
 void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, bool u8) {
-    if (u8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, window_smem_bytes(wp.H), st>>>(wp);
-    else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, window_smem_bytes(wp.H), st>>>(wp);
+    if (u8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, ieds::window_smem_bytes(wp.H), st>>>(wp);
+    else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, ieds::window_smem_bytes(wp.H), st>>>(wp);
 }
 
 template <int C>
@@ -387,7 +386,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     }
     h->c_win = window_size_for(std::max(2, h->c_sat));
     h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) &&
-                   window_smem_bytes(H) <= (size_t)kMaxSmem;
+                   ieds::window_smem_bytes(H) <= (size_t)kMaxSmem;
 
     // frame + (column bitmap for the exact path | two saved rows for the streaming path)
     h->smem_frame = 4ull * (((H + 2) * h->NWP + 3) & ~3) + 8ull * std::max(W, h->NWP);
@@ -412,7 +411,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
-    if (e == cudaSuccess && h->streaming) e = window_attrs(window_smem_bytes(H));
+    if (e == cudaSuccess && h->streaming) e = window_attrs(ieds::window_smem_bytes(H));
     if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);

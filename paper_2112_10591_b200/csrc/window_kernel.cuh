@@ -18,9 +18,9 @@
 // compile-time constant: no stack, no divergence.  The rotations in the middle of the frame
 // (all emitted rows inside the frame) run without any range check; only the first and the
 // last rotation carry them.  Instruction budget per row pair (2 pixels), see DESIGN.md §6:
-//   h of 2 rows   2 x (3 LDS + 2 SHF + BREV + LOP3 + FLO.SH) + 2 x 2 IMAD (packed h^2)
-//   warp vote     2 ISETP + VOTE + BRA (skip the update when no lane has a site < C away)
-//   update        2C VIADDMNMX.U16x2
+//   activity      mask bit test + VOTE + BRA (per-strip pair mask built once after staging)
+//   active only:  h of 2 rows: 3 LDS.64 + 2 x (2 SHF + BREV + LOP3 + FLO.SH) + 4 IMAD (h^2),
+//                 2C VIADDMNMX.U16x2
 //   emit          2 IMAD extracts + 2 LDS (table) + 2 STG + 2 32-bit pointer adds
 #pragma once
 #include <cstdint>
@@ -44,8 +44,14 @@ struct WinParams {
     uint32_t one;                       // 1 (runtime, so 0x10000 = one << 16 stays an IMAD operand)
 };
 
-// rows of dynamic shared memory a CTA stages: H rows plus zero rows for the reads past H
-__host__ __device__ constexpr int window_staged_rows(int H) { return H + kWinMaxC + 1; }
+// row pairs a CTA stages (H rows plus zero rows for the reads past H), and the words of one
+// strip's pair-activity mask (one bit per row pair, plus a zero word for the funnel read)
+__host__ __device__ constexpr int window_staged_pairs(int H) { return (H + kWinMaxC + 2) / 2; }
+__host__ __device__ constexpr int window_mask_words(int H) { return (window_staged_pairs(H) + 31) / 32 + 1; }
+// dynamic shared memory: [pairs][kWinRowWords] uint2 {row 2q, row 2q+1}, then the masks
+__host__ __device__ constexpr size_t window_smem_bytes(int H) {
+    return 8ull * window_staged_pairs(H) * kWinRowWords + 4ull * kWinWarps * window_mask_words(H);
+}
 
 // squared distance x4 from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
 template <int C>
@@ -80,8 +86,7 @@ struct WinState {
     // h of the row at `rp` (this strip's words w-1, w, w+1), clamped to <= 31:
     // clz of (columns x-31..x with x at the MSB) | bitreverse(columns x..x+31) -- the leading
     // zero count of an OR is the min of the two one-sided distances; bit 0 bounds it by 31.
-    __device__ __forceinline__ uint32_t h_of(const uint32_t* rp) const {
-        const uint32_t tl = rp[0], t = rp[1], tr = rp[2];
+    __device__ __forceinline__ uint32_t h_of(uint32_t tl, uint32_t t, uint32_t tr) const {
         const uint32_t left = __funnelshift_rc(tl, t, lane + 1);
         const uint32_t right = __funnelshift_r(t, tr, lane);
         return clz_shiftamt(left | __brev(right) | 1u);
@@ -106,13 +111,14 @@ struct WinState {
     // old logical j+1 min the two parabolas, and the freed register P[S % C] becomes the new
     // last register.  Then pixels y0, y0+1 are final -- a site C or more rows away cannot
     // bring a value below C^2 >= K_sat -- and are emitted.  Slots start at 4*K_sat and only
-    // decrease, so every emitted value is a valid table offset.  `rows` points at row u0 of
-    // the rotation, so both row reads use immediate offsets.
+    // decrease, so every emitted value is a valid table offset.  `pr` points at this strip's
+    // words of pair u0/2 (the rotation's first), so the row reads use immediate offsets; bit S
+    // of `act` says whether rows u, u+1 hold a site fewer than C columns from the strip.
     template <int S, bool FAST>
-    __device__ __forceinline__ void step(const uint32_t* rows, int u0, uint32_t (&P)[C]) {
-        const uint32_t ha = h_of(rows + (2 * S) * kWinRowWords);
-        const uint32_t hb = h_of(rows + (2 * S + 1) * kWinRowWords);   // rows >= H are zero words
-        if (__any_sync(0xFFFFFFFFu, min(ha, hb) < (uint32_t)C)) {
+    __device__ __forceinline__ void step(const uint2* pr, uint32_t act, int u0, uint32_t (&P)[C]) {
+        if (__any_sync(0xFFFFFFFFu, (act >> S) & 1u)) {   // warp-uniform (the mask is per strip)
+            const uint2 wl = pr[S * kWinRowWords], wc = pr[S * kWinRowWords + 1], wr = pr[S * kWinRowWords + 2];
+            const uint32_t ha = h_of(wl.x, wc.x, wr.x), hb = h_of(wl.y, wc.y, wr.y);
             const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
@@ -140,11 +146,11 @@ struct WinState {
     }
 
     template <int S, bool FAST>
-    __device__ __forceinline__ void block(const uint32_t* rows, int u0, int total, uint32_t (&P)[C]) {
+    __device__ __forceinline__ void block(const uint2* pr, uint32_t act, int u0, int total, uint32_t (&P)[C]) {
         if constexpr (S < C) {
             if (FAST || u0 + 2 * S < total) {
-                step<S, FAST>(rows, u0, P);
-                block<S + 1, FAST>(rows, u0, total, P);
+                step<S, FAST>(pr, act, u0, P);
+                block<S + 1, FAST>(pr, act, u0, total, P);
             }
         }
     }
@@ -154,24 +160,27 @@ template <int C, typename OutT>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
     static_assert(C >= 2 && C <= kWinMaxC, "window size (h is clamped to 31)");
     __shared__ uint32_t lut_s[kWinLutMax + 1];           // table, raw output bit patterns
-    extern __shared__ __align__(16) uint32_t wsm[];      // [H + kWinMaxC + 1][kWinRowWords] E_df words
+    extern __shared__ __align__(16) uint32_t wsm[];      // row pairs of E_df words, then the masks
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
     const int NWP2 = p.NW + 2;
+    const int NPS = window_staged_pairs(H), MW = window_mask_words(H);
+    const uint2* pairs = reinterpret_cast<const uint2*>(wsm);
+    uint32_t* masks = wsm + 2 * NPS * kWinRowWords;
     // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
-    // plus zero rows past the end for the reads of the last rotation: asynchronous 4-byte
-    // copies, zero-filled where out of range, all in flight at once
+    // plus zero rows past the end, interleaved by row pair: asynchronous 4-byte copies,
+    // zero-filled where out of range, all in flight at once
     {
         const uint32_t* src = p.Edf + (size_t)b * H * NWP2 + w0;
         constexpr int kRowsPerPass = (kWinWarps * 32) / kWinRowWords;   // 25 rows x 10 words
         const int c = threadIdx.x % kWinRowWords, y_first = threadIdx.x / kWinRowWords;
         const bool col_ok = w0 + c < NWP2;
-        const int rows_staged = window_staged_rows(H);
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(wsm);
         if (y_first < kRowsPerPass) {
-            uint32_t dst = (uint32_t)__cvta_generic_to_shared(wsm + y_first * kWinRowWords + c);
-            for (int y = y_first; y < rows_staged; y += kRowsPerPass, dst += 4u * kRowsPerPass * kWinRowWords) {
+            for (int y = y_first; y < 2 * NPS; y += kRowsPerPass) {
                 const bool ok = col_ok && y < H;
                 const uint32_t* g = ok ? src + (size_t)y * NWP2 + c : src;
+                const uint32_t dst = base + 8u * (uint32_t)((y >> 1) * kWinRowWords + c) + 4u * (uint32_t)(y & 1);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(g), "r"(ok ? 4 : 0)
                              : "memory");
             }
@@ -187,6 +196,26 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
 
     const int w = w0 + warp;
     if (w >= p.NW) return;
+    // pair-activity mask of this strip: bit q = rows 2q, 2q+1 hold a set pixel in columns
+    // [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane has h < C there (exactly the lanes' test)
+    uint32_t* msk = masks + warp * MW;
+    {
+        constexpr uint32_t kLeft = ~0u << (33 - C);        // columns 32w-(C-1) .. 32w-1 of word w-1
+        constexpr uint32_t kRight = (1u << (C - 1)) - 1u;  // columns 32w+32 .. 32w+30+C of word w+1
+        for (int i = 0; i < MW; ++i) {
+            const int q = 32 * i + lane;
+            uint32_t any = 0u;
+            if (q < NPS) {
+                const uint2 a = pairs[q * kWinRowWords + warp], m = pairs[q * kWinRowWords + warp + 1],
+                            r = pairs[q * kWinRowWords + warp + 2];
+                any = ((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight);
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
+            if (lane == 0) msk[i] = bal;
+        }
+        __syncwarp();
+    }
+
     const int x = 32 * w + lane;
     WinState<C, OutT> st;
     st.H = H;
@@ -205,7 +234,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     // window must lie inside one 4 GB-aligned range (else all rotations take the checked path)
     const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(H - 1);
     const bool fast_ok = __all_sync(0xFFFFFFFFu, (last >> 32) == (st.op >> 32));
-    const uint32_t* rows = wsm + warp;   // this strip's words w-1, w, w+1 of row 0
+    const uint2* pr = pairs + warp;   // this strip's words w-1, w, w+1 of pair 0
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
     uint32_t P[C];
@@ -215,10 +244,12 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     // rotation 0 emits rows y0 < 0 (skipped); a rotation u0 >= 2C with u0 + C < H emits only
     // rows inside the frame and reads only staged rows: no checks there
     for (int u0 = 0; u0 < total; u0 += 2 * C) {
+        const int q0 = u0 >> 1;
+        const uint32_t act = __funnelshift_r(msk[q0 >> 5], msk[(q0 >> 5) + 1], q0 & 31);
         if (fast_ok && u0 >= 2 * C && u0 + C < H)
-            st.template block<0, true>(rows + u0 * kWinRowWords, u0, total, P);
+            st.template block<0, true>(pr + q0 * kWinRowWords, act, u0, total, P);
         else
-            st.template block<0, false>(rows + u0 * kWinRowWords, u0, total, P);
+            st.template block<0, false>(pr + q0 * kWinRowWords, act, u0, total, P);
     }
 }
 
