@@ -18,7 +18,7 @@
 // compile-time constant: no stack, no divergence.  The rotations in the middle of the frame
 // (all emitted rows inside the frame) run without any range check; only the first and the
 // last rotation carry them.  Instruction budget per row pair (2 pixels), see DESIGN.md §6:
-//   activity      mask bit test + VOTE + BRA (per-strip pair mask built once after staging)
+//   activity      uniform bit test + BRA (one ballot per rotation gives the C pair bits)
 //   active only:  h of 2 rows: 3 LDS.64 + 2 x (2 SHF + BREV + LOP3 + FLO.SH) + 4 IMAD (h^2),
 //                 2C VIADDMNMX.U16x2
 //   emit          2 IMAD extracts + 2 LDS (table) + 2 STG + 2 32-bit pointer adds
@@ -44,14 +44,11 @@ struct WinParams {
     uint32_t one;                       // 1 (runtime, so 0x10000 = one << 16 stays an IMAD operand)
 };
 
-// row pairs a CTA stages (H rows plus zero rows for the reads past H), and the words of one
-// strip's pair-activity mask (one bit per row pair, plus a zero word for the funnel read)
-__host__ __device__ constexpr int window_staged_pairs(int H) { return (H + kWinMaxC + 2) / 2; }
-__host__ __device__ constexpr int window_mask_words(int H) { return (window_staged_pairs(H) + 31) / 32 + 1; }
-// dynamic shared memory: [pairs][kWinRowWords] uint2 {row 2q, row 2q+1}, then the masks
-__host__ __device__ constexpr size_t window_smem_bytes(int H) {
-    return 8ull * window_staged_pairs(H) * kWinRowWords + 4ull * kWinWarps * window_mask_words(H);
-}
+// row pairs a CTA stages: H rows plus zero rows for the reads past H (steps read pairs
+// q < (H + C) / 2)
+__host__ __device__ constexpr int window_staged_pairs(int H) { return (H + 2 * kWinMaxC + 2) / 2; }
+// dynamic shared memory: [pairs][kWinRowWords] uint2 {row 2q, row 2q+1}
+__host__ __device__ constexpr size_t window_smem_bytes(int H) { return 8ull * window_staged_pairs(H) * kWinRowWords; }
 
 // squared distance x4 from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
 template <int C>
@@ -116,7 +113,7 @@ struct WinState {
     // of `act` says whether rows u, u+1 hold a site fewer than C columns from the strip.
     template <int S, bool FAST>
     __device__ __forceinline__ void step(const uint2* pr, uint32_t act, int u0, uint32_t (&P)[C]) {
-        if (__any_sync(0xFFFFFFFFu, (act >> S) & 1u)) {   // warp-uniform (the mask is per strip)
+        if (act & (1u << S)) {   // warp-uniform: a ballot result
             const uint2 wl = pr[S * kWinRowWords], wc = pr[S * kWinRowWords + 1], wr = pr[S * kWinRowWords + 2];
             const uint32_t ha = h_of(wl.x, wc.x, wr.x), hb = h_of(wl.y, wc.y, wr.y);
             const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
@@ -160,13 +157,12 @@ template <int C, typename OutT>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
     static_assert(C >= 2 && C <= kWinMaxC, "window size (h is clamped to 31)");
     __shared__ uint32_t lut_s[kWinLutMax + 1];           // table, raw output bit patterns
-    extern __shared__ __align__(16) uint32_t wsm[];      // row pairs of E_df words, then the masks
+    extern __shared__ __align__(16) uint32_t wsm[];      // row pairs of E_df words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
     const int NWP2 = p.NW + 2;
-    const int NPS = window_staged_pairs(H), MW = window_mask_words(H);
+    const int NPS = window_staged_pairs(H);
     const uint2* pairs = reinterpret_cast<const uint2*>(wsm);
-    uint32_t* masks = wsm + 2 * NPS * kWinRowWords;
     // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
     // plus zero rows past the end, interleaved by row pair: asynchronous 4-byte copies,
     // zero-filled where out of range, all in flight at once
@@ -196,26 +192,6 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
 
     const int w = w0 + warp;
     if (w >= p.NW) return;
-    // pair-activity mask of this strip: bit q = rows 2q, 2q+1 hold a set pixel in columns
-    // [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane has h < C there (exactly the lanes' test)
-    uint32_t* msk = masks + warp * MW;
-    {
-        constexpr uint32_t kLeft = ~0u << (33 - C);        // columns 32w-(C-1) .. 32w-1 of word w-1
-        constexpr uint32_t kRight = (1u << (C - 1)) - 1u;  // columns 32w+32 .. 32w+30+C of word w+1
-        for (int i = 0; i < MW; ++i) {
-            const int q = 32 * i + lane;
-            uint32_t any = 0u;
-            if (q < NPS) {
-                const uint2 a = pairs[q * kWinRowWords + warp], m = pairs[q * kWinRowWords + warp + 1],
-                            r = pairs[q * kWinRowWords + warp + 2];
-                any = ((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight);
-            }
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
-            if (lane == 0) msk[i] = bal;
-        }
-        __syncwarp();
-    }
-
     const int x = 32 * w + lane;
     WinState<C, OutT> st;
     st.H = H;
@@ -235,17 +211,29 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(H - 1);
     const bool fast_ok = __all_sync(0xFFFFFFFFu, (last >> 32) == (st.op >> 32));
     const uint2* pr = pairs + warp;   // this strip's words w-1, w, w+1 of pair 0
+    constexpr uint32_t kLeft = ~0u << (33 - C);        // columns 32w-(C-1) .. 32w-1 of word w-1
+    constexpr uint32_t kRight = (1u << (C - 1)) - 1u;  // columns 32w+32 .. 32w+30+C of word w+1
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
     uint32_t P[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) P[k] = st.ksat4x2;
     const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
+    const int npairs = (total + 1) >> 1;
     // rotation 0 emits rows y0 < 0 (skipped); a rotation u0 >= 2C with u0 + C < H emits only
     // rows inside the frame and reads only staged rows: no checks there
     for (int u0 = 0; u0 < total; u0 += 2 * C) {
         const int q0 = u0 >> 1;
-        const uint32_t act = __funnelshift_r(msk[q0 >> 5], msk[(q0 >> 5) + 1], q0 & 31);
+        // activity of the rotation's C row pairs, lane j < C testing pair q0 + j: rows 2q, 2q+1
+        // hold a set pixel in columns [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane has
+        // h < C there (exactly the lanes' own test); staged rows past H read as zero
+        uint32_t any = 0u;
+        if (lane < C && q0 + lane < npairs) {
+            const uint2* q = pr + (q0 + lane) * kWinRowWords;
+            const uint2 a = q[0], m = q[1], r = q[2];
+            any = ((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight);
+        }
+        const uint32_t act = __ballot_sync(0xFFFFFFFFu, any != 0u);
         if (fast_ok && u0 >= 2 * C && u0 + C < H)
             st.template block<0, true>(pr + q0 * kWinRowWords, act, u0, total, P);
         else
