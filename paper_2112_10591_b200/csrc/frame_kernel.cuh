@@ -6,11 +6,12 @@
 //   then         E_df is transposed into column words T (bit i of T[r][x] = E_df(x, 32r+i))
 //                plus a per-column bitmap of non-empty word-rows, which is all the EDT needs.
 //
-// Layout: the frame lives in shared memory as H + 2 rows of NWP words, NWP = the smallest odd
+// Layout: the frame lives in shared memory as H + 3 rows of NWP words, NWP = the smallest odd
 // number > ceil(W/32) (an odd row stride makes the "lane = row" accesses bank-conflict free and
-// leaves at least one zero pad word per row).  Frame row y is shared row y + 1; rows 0 and H+1
-// and the pad words are zero, so out-of-frame neighbours read as non-edge (reading R1) without
-// bounds checks.  Bit (x % 32) of word x / 32 is pixel x; bits beyond W stay 0.
+// leaves at least one zero pad word per row), after 4 zero words (so word -1 of row -1 reads 0).
+// Frame row y is shared row y + 1; rows 0, H+1, H+2 and the pad words are zero, so
+// out-of-frame neighbours read as non-edge (reading R1) without bounds checks.  Bit (x % 32) of
+// word x / 32 is pixel x; bits beyond W stay 0.
 #pragma once
 #include <cstdint>
 
@@ -62,14 +63,14 @@ __device__ __forceinline__ uint32_t denoised_word(const uint32_t* fr, const Fram
     return c & at_least(p.n_d, up, dn, lf, rt);
 }
 
-// returns 1 if the event is outside the frame
-__device__ __forceinline__ uint32_t scatter_event(uint32_t* fr, const FrameParams& p, uint32_t v) {
-    uint32_t x = v & 0xFFFFu, y = v >> 16;
-    if (x < (uint32_t)p.W && y < (uint32_t)p.H) {
-        atomicOr(&fr[(y + 1) * p.NWP + (x >> 5)], 1u << (x & 31));
-        return 0u;
-    }
-    return 1u;
+// Sets the event's pixel; returns nonzero if the event is outside the frame.  Branch-free: the
+// coordinates are clamped into the frame with one packed min (lim = (H-1) << 16 | (W-1)) and an
+// out-of-frame event ORs nothing.
+__device__ __forceinline__ uint32_t scatter_event(uint32_t* fr1, uint32_t lim, int NWP, uint32_t v) {
+    const uint32_t c = __vminu2(v, lim);
+    const uint32_t x = c & 0xFFFFu, y = c >> 16;
+    atomicOr(&fr1[y * NWP + (x >> 5)], c == v ? 1u << (x & 31) : 0u);
+    return c ^ v;
 }
 
 __device__ __forceinline__ uint4 ld_stream_u4(const uint4* ptr) {
@@ -104,104 +105,113 @@ __device__ __forceinline__ uint32_t stencil_word(const uint32_t* fr, int i, int 
     return at_least(N, fr[i - NWP], fr[i + NWP], lf, rt);
 }
 
-constexpr int kDfWords = 16;   // frame words staged per thread per round of the in-place pass
+// (a & 0x80000000) | (b & 0x7FFFFFFF): bit 31 from a, the rest from b (one LOP3)
+__device__ __forceinline__ uint32_t sel31(uint32_t a, uint32_t b) { return (a & 0x80000000u) | (b & 0x7FFFFFFFu); }
 
-// Alg. 1 in place (E -> E_d) in rounds of row bands whose E_d words are staged in registers
-// between barriers; the last E row of a band is saved before it is overwritten, because the
-// next band's first row needs it as its upper neighbour.  Then Alg. 2 reads E_d and writes
-// the row-major E_df scratch (word w of row y at [y][1 + w]; the guard words stay 0).
-// sv: 2 * NWP words of shared scratch for the saved rows.
-template <int ND, int NF>
-__device__ __forceinline__ void denoise_fill_inplace(uint32_t* fr, uint32_t* sv, const FrameParams& p, int b,
-                                                     int tid, int nthr) {
-    const int NWP = p.NWP, H = p.H;
-    const int rows_per_round = max(1, (kDfWords * nthr) / NWP);
-    uint32_t* prevE = sv;          // E of the row above the current band (zeros for band 0)
-    uint32_t* saveE = sv + NWP;
-    for (int i = tid; i < NWP; i += nthr) prevE[i] = 0u;
-    __syncthreads();
-    for (int r0 = 0; r0 < H; r0 += rows_per_round) {
-        const int r1 = min(H, r0 + rows_per_round);
-        const int lo = (r0 + 1) * NWP, hi = (r1 + 1) * NWP;
-        uint32_t ed[kDfWords];
-#pragma unroll
-        for (int k = 0; k < kDfWords; ++k) {
-            const int i = lo + tid + k * nthr;
-            uint32_t v = 0u;
-            if (i < hi) {
-                const uint32_t c = fr[i];
-                const uint32_t up = (i < lo + NWP) ? prevE[i - lo] : fr[i - NWP];
-                const uint32_t lf = (c << 1) | (fr[i - 1] >> 31);
-                const uint32_t rt = (c >> 1) | (fr[i + 1] << 31);
-                v = c & at_least(ND, up, fr[i + NWP], lf, rt);
-            }
-            ed[k] = v;
-        }
-        for (int i = tid; i < NWP; i += nthr) saveE[i] = fr[(r1 - 1 + 1) * NWP + i];
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kDfWords; ++k) {
-            const int i = lo + tid + k * nthr;
-            if (i < hi) fr[i] = ed[k];
-        }
-        uint32_t* t = prevE;
-        prevE = saveE;
-        saveE = t;
-        __syncthreads();
-    }
-    const uint32_t lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : kFull;
+// E rows of one word column and its neighbours: l = word w-1, c = word w, r = word w+1
+struct Row3 {
+    uint32_t l, c, r;
+};
+
+// E_d (Alg. 1) of row r from E rows r-1 (a), r (m), r+1 (n):
+//   d = word w;  s = bit 31: pixel 31 of word w-1, bit 0: pixel 0 of word w+1 (other bits junk)
+template <int ND>
+__device__ __forceinline__ void denoise_row(const Row3& a, const Row3& m, const Row3& n, uint32_t& d, uint32_t& s) {
+    d = m.c & at_least(ND, a.c, n.c, __funnelshift_l(m.l, m.c, 1), __funnelshift_r(m.c, m.r, 1));
+    // the neighbours of pixel 31 of word w-1 (bit 31) and of pixel 0 of word w+1 (bit 0):
+    // left of (w-1, 31) is (w-1, 30); left of (w+1, 0) is (w, 31); right of (w-1, 31) is
+    // (w, 0); right of (w+1, 0) is (w+1, 1)
+    s = sel31(m.l, m.r) & at_least(ND, sel31(a.l, a.r), sel31(n.l, n.r), sel31(m.l << 1, m.c >> 31),
+                                   sel31(m.c << 31, m.r >> 1));
+}
+
+// Alg. 1 then Alg. 2 for word column w of rows [y0, y1), fused as one top-to-bottom walk over
+// the read-only E frame: E rows y-1..y+2 and E_d rows y-1..y+1 live in registers, each step
+// loads one E row (3 words) and writes one E_df word.  fr1 = shared row 1 (frame row 0).
+template <int ND, int NF, bool DBG>
+__device__ __forceinline__ void df_walk(const uint32_t* fr1, const FrameParams& p, int b, int w, int y0, int y1,
+                                        uint32_t wmask) {
+    const int NWP = p.NWP;
+    const uint32_t* q = fr1 + y0 * NWP + w;   // frame row y0, word w
+    auto ld = [&](int dr) {                   // E row y0 + dr (rows -1, H, H+1 are zero guards)
+        const uint32_t* t = q + dr * NWP;
+        return Row3{t[-1], t[0], t[1]};
+    };
+    Row3 e0 = y0 > 0 ? ld(-2) : Row3{0u, 0u, 0u};   // row -2 does not exist: E_d(-1) = 0 anyway
+    Row3 e1 = ld(-1), e2 = ld(0), e3 = ld(1);
+    uint32_t dP, sP, dC, sC;
+    denoise_row<ND>(e0, e1, e2, dP, sP);   // E_d(y0 - 1) (only its word w is used)
+    denoise_row<ND>(e1, e2, e3, dC, sC);   // E_d(y0)
+    Row3 eA = e2, eB = e3;                 // E rows y, y+1
     const size_t NW2 = (size_t)p.NW + 2;
-    uint32_t* scratch = p.Edf_scratch + (size_t)b * H * NW2;
-    const int n = H * NWP;
-    // (y, w) of index j advanced incrementally (no division in the loop)
-    const int dy = nthr / NWP, dw = nthr - (nthr / NWP) * NWP;
-    int y = tid / NWP, w = tid - (tid / NWP) * NWP;
-    for (int j = tid; j < n; j += nthr, y += dy, w += dw) {
-        if (w >= NWP) {
-            w -= NWP;
-            ++y;
+    uint32_t* out = p.Edf_scratch + ((size_t)b * p.H + y0) * NW2 + 1 + w;
+    const uint32_t* qn = q + 2 * NWP;      // E row y + 2
+    for (int y = y0; y < y1; ++y) {
+        const Row3 eN{qn[-1], qn[0], qn[1]};
+        qn += NWP;
+        uint32_t dN, sN;
+        denoise_row<ND>(eA, eB, eN, dN, sN);   // E_d(y + 1)
+        const uint32_t df =
+            (dC | at_least(NF, dP, dN, __funnelshift_l(sC, dC, 1), __funnelshift_r(dC, sC, 1))) & wmask;
+        *out = df;
+        out += NW2;
+        if constexpr (DBG) {
+            const size_t o = ((size_t)b * p.H + y) * p.NW + w;
+            if (p.Ed_out) p.Ed_out[o] = dC;
+            if (p.Edf_out) p.Edf_out[o] = df;
         }
-        if (w >= p.NW) continue;
-        const int i = j + NWP;
-        const uint32_t c = fr[i];
-        const uint32_t lf = (c << 1) | (fr[i - 1] >> 31);
-        const uint32_t rt = (c >> 1) | (fr[i + 1] << 31);
-        uint32_t df = c | at_least(NF, fr[i - NWP], fr[i + NWP], lf, rt);
-        if (w == p.NW - 1) df &= lastmask;
-        scratch[(size_t)y * NW2 + 1 + w] = df;
-        const size_t o = ((size_t)b * H + y) * p.NW + w;
-        if (p.Ed_out) p.Ed_out[o] = c;
-        if (p.Edf_out) p.Edf_out[o] = df;
+        dP = dC;
+        dC = dN;
+        sC = sN;
+        eA = eB;
+        eB = eN;
     }
+}
+
+// the default path's a2 + a3: word columns x row bands over the CTA's threads
+template <int ND, int NF>
+__device__ __forceinline__ void denoise_fill_walk(const uint32_t* fr1, const FrameParams& p, int b, int tid,
+                                                  int nthr) {
+    const int NW = p.NW, H = p.H;
+    const int nbands = nthr / NW;   // >= 1 (host: NW <= threads)
+    const int band = tid / NW, w = tid - band * NW;
+    if (band >= nbands) return;
+    const int rows = (H + nbands - 1) / nbands;
+    const int y0 = band * rows, y1 = min(H, y0 + rows);
+    if (y0 >= y1) return;
+    const uint32_t wmask = (w == NW - 1 && (p.W & 31)) ? ((1u << (p.W & 31)) - 1u) : kFull;
+    if (p.Ed_out || p.Edf_out)
+        df_walk<ND, NF, true>(fr1, p, b, w, y0, y1, wmask);
+    else
+        df_walk<ND, NF, false>(fr1, p, b, w, y0, y1, wmask);
 }
 
 template <int ND>
-__device__ __forceinline__ void denoise_fill_nf(uint32_t* fr, uint32_t* sv, const FrameParams& p, int b, int tid,
-                                                int nthr) {
+__device__ __forceinline__ void denoise_fill_nf(const uint32_t* fr1, const FrameParams& p, int b, int tid, int nthr) {
     switch (p.n_f) {
-        case 1: denoise_fill_inplace<ND, 1>(fr, sv, p, b, tid, nthr); break;
-        case 2: denoise_fill_inplace<ND, 2>(fr, sv, p, b, tid, nthr); break;
-        case 3: denoise_fill_inplace<ND, 3>(fr, sv, p, b, tid, nthr); break;
-        case 4: denoise_fill_inplace<ND, 4>(fr, sv, p, b, tid, nthr); break;
-        default: denoise_fill_inplace<ND, 5>(fr, sv, p, b, tid, nthr); break;
+        case 1: denoise_fill_walk<ND, 1>(fr1, p, b, tid, nthr); break;
+        case 2: denoise_fill_walk<ND, 2>(fr1, p, b, tid, nthr); break;
+        case 3: denoise_fill_walk<ND, 3>(fr1, p, b, tid, nthr); break;
+        case 4: denoise_fill_walk<ND, 4>(fr1, p, b, tid, nthr); break;
+        default: denoise_fill_walk<ND, 5>(fr1, p, b, tid, nthr); break;
     }
 }
 
-__device__ __forceinline__ void streaming_denoise_fill(uint32_t* fr, uint32_t* sv, const FrameParams& p, int b,
-                                                       int tid, int nthr) {
+__device__ __forceinline__ void streaming_denoise_fill(const uint32_t* fr1, const FrameParams& p, int b, int tid,
+                                                       int nthr) {
     switch (p.n_d) {
-        case 0: denoise_fill_nf<0>(fr, sv, p, b, tid, nthr); break;
-        case 1: denoise_fill_nf<1>(fr, sv, p, b, tid, nthr); break;
-        case 2: denoise_fill_nf<2>(fr, sv, p, b, tid, nthr); break;
-        case 3: denoise_fill_nf<3>(fr, sv, p, b, tid, nthr); break;
-        default: denoise_fill_nf<4>(fr, sv, p, b, tid, nthr); break;
+        case 0: denoise_fill_nf<0>(fr1, p, b, tid, nthr); break;
+        case 1: denoise_fill_nf<1>(fr1, p, b, tid, nthr); break;
+        case 2: denoise_fill_nf<2>(fr1, p, b, tid, nthr); break;
+        case 3: denoise_fill_nf<3>(fr1, p, b, tid, nthr); break;
+        default: denoise_fill_nf<4>(fr1, p, b, tid, nthr); break;
     }
 }
 
 __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    const int nframe = (p.H + 2) * p.NWP;
-    uint32_t* fr = smem;
+    const int nframe = 4 + (p.H + 3) * p.NWP;   // 4 zero words, then the frame (see Layout)
+    uint32_t* fr = smem + 4;
     unsigned long long* cm = reinterpret_cast<unsigned long long*>(smem + ((nframe + 3) & ~3));
     const int b = blockIdx.x;
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -224,28 +234,31 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
         o0 = o1 = 0;
     }
     uint32_t bad = 0;
+    uint32_t* fr1 = fr + p.NWP;   // frame row 0
+    const uint32_t lim = ((uint32_t)(p.H - 1) << 16) | (uint32_t)(p.W - 1);
+    const int NWP = p.NWP;
     if (p.vec_ok) {
         int64_t h1 = o1 < ((o0 + 3) & ~3ll) ? o1 : ((o0 + 3) & ~3ll);
         int64_t v1 = h1 > (o1 & ~3ll) ? h1 : (o1 & ~3ll);
-        for (int64_t i = o0 + tid; i < h1; i += nthr) bad |= scatter_event(fr, p, __ldg(p.xy + i));
+        for (int64_t i = o0 + tid; i < h1; i += nthr) bad |= scatter_event(fr1, lim, NWP, __ldg(p.xy + i));
         const uint4* x4 = reinterpret_cast<const uint4*>(p.xy);
         int64_t j = (h1 >> 2) + tid;
         const int64_t j1 = v1 >> 2;
         for (; j + 3 * nthr < j1; j += 4 * nthr) {   // 4 loads in flight per thread
             uint4 q0 = ld_stream_u4(x4 + j), q1 = ld_stream_u4(x4 + j + nthr);
             uint4 q2 = ld_stream_u4(x4 + j + 2 * nthr), q3 = ld_stream_u4(x4 + j + 3 * nthr);
-            bad |= scatter_event(fr, p, q0.x) | scatter_event(fr, p, q0.y) | scatter_event(fr, p, q0.z) | scatter_event(fr, p, q0.w);
-            bad |= scatter_event(fr, p, q1.x) | scatter_event(fr, p, q1.y) | scatter_event(fr, p, q1.z) | scatter_event(fr, p, q1.w);
-            bad |= scatter_event(fr, p, q2.x) | scatter_event(fr, p, q2.y) | scatter_event(fr, p, q2.z) | scatter_event(fr, p, q2.w);
-            bad |= scatter_event(fr, p, q3.x) | scatter_event(fr, p, q3.y) | scatter_event(fr, p, q3.z) | scatter_event(fr, p, q3.w);
+            bad |= scatter_event(fr1, lim, NWP, q0.x) | scatter_event(fr1, lim, NWP, q0.y) | scatter_event(fr1, lim, NWP, q0.z) | scatter_event(fr1, lim, NWP, q0.w);
+            bad |= scatter_event(fr1, lim, NWP, q1.x) | scatter_event(fr1, lim, NWP, q1.y) | scatter_event(fr1, lim, NWP, q1.z) | scatter_event(fr1, lim, NWP, q1.w);
+            bad |= scatter_event(fr1, lim, NWP, q2.x) | scatter_event(fr1, lim, NWP, q2.y) | scatter_event(fr1, lim, NWP, q2.z) | scatter_event(fr1, lim, NWP, q2.w);
+            bad |= scatter_event(fr1, lim, NWP, q3.x) | scatter_event(fr1, lim, NWP, q3.y) | scatter_event(fr1, lim, NWP, q3.z) | scatter_event(fr1, lim, NWP, q3.w);
         }
         for (; j < j1; j += nthr) {
             uint4 q = ld_stream_u4(x4 + j);
-            bad |= scatter_event(fr, p, q.x) | scatter_event(fr, p, q.y) | scatter_event(fr, p, q.z) | scatter_event(fr, p, q.w);
+            bad |= scatter_event(fr1, lim, NWP, q.x) | scatter_event(fr1, lim, NWP, q.y) | scatter_event(fr1, lim, NWP, q.z) | scatter_event(fr1, lim, NWP, q.w);
         }
-        for (int64_t i = v1 + tid; i < o1; i += nthr) bad |= scatter_event(fr, p, __ldg(p.xy + i));
+        for (int64_t i = v1 + tid; i < o1; i += nthr) bad |= scatter_event(fr1, lim, NWP, __ldg(p.xy + i));
     } else {
-        for (int64_t i = o0 + tid; i < o1; i += nthr) bad |= scatter_event(fr, p, __ldg(p.xy + i));
+        for (int64_t i = o0 + tid; i < o1; i += nthr) bad |= scatter_event(fr1, lim, NWP, __ldg(p.xy + i));
     }
     if (bad) atomicOr(p.err, kErrRange);
     __syncthreads();
@@ -256,7 +269,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
     }
 
     if (!p.T) {   // streaming surface path: row-major E_df only
-        streaming_denoise_fill(fr, reinterpret_cast<uint32_t*>(cm), p, b, tid, nthr);
+        streaming_denoise_fill(fr1, p, b, tid, nthr);
         return;
     }
 

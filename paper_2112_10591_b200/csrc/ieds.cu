@@ -388,12 +388,12 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) &&
                    ieds::window_smem_bytes(H) <= (size_t)kMaxSmem;
 
-    // frame + (column bitmap for the exact path | two saved rows for the streaming path)
-    h->smem_frame = 4ull * (((H + 2) * h->NWP + 3) & ~3) + 8ull * std::max(W, h->NWP);
+    // 4 zero words + frame (H + 3 rows), then the column bitmap of the exact path
+    h->smem_frame = 4ull * ((4 + (H + 3) * h->NWP + 3) & ~3) + 8ull * std::max(W, h->NWP);
     h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
     h->smem_edt_d2 = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, true);
     if (h->smem_frame > (size_t)kMaxSmem || h->smem_edt_d2 > (size_t)kMaxSmem || h->SEGW > 255 ||
-        h->NWP > ieds::kDfWords * kFrameThreads) {
+        h->NW > kFrameThreads) {   // the D&F walk gives every word column a thread
         delete h;
         return IEDS_EINVAL;
     }
