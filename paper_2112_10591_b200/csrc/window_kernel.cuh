@@ -102,54 +102,77 @@ struct WinState {
         }
     }
 
-    // Rotating window: before a pair step of phase S, logical register j (pixels y0+2j,
-    // y0+2j+1 with y0 = u-C+1) lives in P[(j + S) % C].  The step applies the sites of rows
-    // u, u+1 and shifts the window by one register, in place: logical j of the new window is
-    // old logical j+1 min the two parabolas, and the freed register P[S % C] becomes the new
-    // last register.  Then pixels y0, y0+1 are final -- a site C or more rows away cannot
-    // bring a value below C^2 >= K_sat -- and are emitted.  Slots start at 4*K_sat and only
-    // decrease, so every emitted value is a valid table offset.  `pr` points at this strip's
-    // words of pair u0/2 (the rotation's first), so the row reads use immediate offsets; bit S
-    // of `act` says whether rows u, u+1 hold a site fewer than C columns from the strip.
-    template <int S, bool FAST>
-    __device__ __forceinline__ void step(const uint2* pr, uint32_t act, int u0, uint32_t (&P)[C]) {
+    // Rotating window (steady state): before a pair step of phase S, logical register j
+    // (pixels y0+2j, y0+2j+1 with y0 = u-C+1) lives in P[(j + S) % C].  The step applies the
+    // sites of rows u, u+1 and shifts the window by one register, in place: logical j of the
+    // new window is old logical j+1 min the two parabolas, and the freed register P[S % C]
+    // becomes the new last register.  Then pixels y0, y0+1 are final -- a site C or more rows
+    // away cannot bring a value below C^2 >= K_sat -- and are emitted.  Slots start at 4*K_sat
+    // and only decrease, so every emitted value is a valid table offset.  `pr` points at this
+    // strip's words of pair u0/2 (the rotation's first), so the row reads use immediate
+    // offsets; bit S of `act` says whether rows u, u+1 hold a site fewer than C columns from
+    // the strip.  All emitted rows lie inside the frame (the caller guarantees it).
+    template <int S>
+    __device__ __forceinline__ void step(const uint2* pr, uint32_t act, uint32_t (&P)[C]) {
         if (act & (1u << S)) {   // warp-uniform: a ballot result
             const uint2 wl = pr[S * kWinRowWords], wc = pr[S * kWinRowWords + 1], wr = pr[S * kWinRowWords + 2];
             const uint32_t ha = h_of(wl.x, wc.x, wr.x), hb = h_of(wl.y, wc.y, wr.y);
             const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
-                const uint32_t sqa = dsq4<C>(2 * j, 0) | (dsq4<C>(2 * j + 1, 0) << 16);
-                const uint32_t sqb = dsq4<C>(2 * j, 1) | (dsq4<C>(2 * j + 1, 1) << 16);
                 const int m = (j + S + 1) % C;
                 const uint32_t prev = (j + 1 < C) ? P[m] : ksat4x2;
                 // two fused packed add+min: no carries cross the halves because every sum
                 // stays below 4 * (31^2 + 31^2) < 2^16
-                P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sqa)), __vadd2(h2b, sqb));
+                P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sq2<0>(j))), __vadd2(h2b, sq2<1>(j)));
             }
         } else {
             P[S % C] = ksat4x2;   // the new last register starts empty
         }
         const uint32_t v = P[(S + 1) % C];
         const uint32_t hi = __umulhi(v, k65536), lo = v - hi * 0x10000u;
-        if constexpr (!FAST) {
-            const int y0 = u0 + 2 * S - (C - 1);
-            if (y0 >= 0 && y0 < H) emit<false>(lo);
-            if (y0 + 1 >= 0 && y0 + 1 < H) emit<false>(hi);
-        } else {
-            emit<true>(lo);
-            emit<true>(hi);
+        emit<true>(lo);
+        emit<true>(hi);
+    }
+
+    template <int S>
+    __device__ __forceinline__ void rotation(const uint2* pr, uint32_t act, uint32_t (&P)[C]) {
+        if constexpr (S < C) {
+            step<S>(pr, act, P);
+            rotation<S + 1>(pr, act, P);
         }
     }
 
-    template <int S, bool FAST>
-    __device__ __forceinline__ void block(const uint2* pr, uint32_t act, int u0, int total, uint32_t (&P)[C]) {
-        if constexpr (S < C) {
-            if (FAST || u0 + 2 * S < total) {
-                step<S, FAST>(pr, act, u0, P);
-                block<S + 1, FAST>(pr, act, u0, total, P);
+    // One pair step outside the steady state (the first rows, the last rows, or every row when
+    // the fast address stepping is not allowed): a rolled loop body that keeps logical j in
+    // P[j] by shifting the registers explicitly, checks the emitted rows against the frame and
+    // steps the full 64-bit address.  Its code is one step long, so the hot rotation above is
+    // the only large body in the instruction cache.
+    __device__ __forceinline__ void step_rolled(const uint2* pq, int u, uint32_t (&P)[C]) {
+        const uint2 wl = pq[0], wc = pq[1], wr = pq[2];
+        const uint32_t ha = h_of(wl.x, wc.x, wr.x), hb = h_of(wl.y, wc.y, wr.y);
+        if (__any_sync(0xFFFFFFFFu, min(ha, hb) < (uint32_t)C)) {
+            const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
+#pragma unroll
+            for (int j = 0; j < C; ++j) {
+                const uint32_t prev = (j + 1 < C) ? P[j + 1] : ksat4x2;
+                P[j] = __vminu2(__vminu2(prev, __vadd2(h2a, sq2<0>(j))), __vadd2(h2b, sq2<1>(j)));
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < C; ++j) P[j] = (j + 1 < C) ? P[j + 1] : ksat4x2;
         }
+        const uint32_t v = P[0];
+        const uint32_t hi = __umulhi(v, k65536), lo = v - hi * 0x10000u;
+        const int y0 = u - (C - 1);
+        if (y0 >= 0 && y0 < H) emit<false>(lo);
+        if (y0 + 1 >= 0 && y0 + 1 < H) emit<false>(hi);
+    }
+
+    // packed squared distances x4 from row u + R of a pair to pixels y0 + 2j, y0 + 2j + 1
+    template <int R>
+    __device__ __forceinline__ static constexpr uint32_t sq2(int j) {
+        return dsq4<C>(2 * j, R) | (dsq4<C>(2 * j + 1, R) << 16);
     }
 };
 
@@ -220,25 +243,27 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     for (int k = 0; k < C; ++k) P[k] = st.ksat4x2;
     const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
     const int npairs = (total + 1) >> 1;
-    // rotation 0 emits rows y0 < 0 (skipped); a rotation u0 >= 2C with u0 + C < H emits only
-    // rows inside the frame and reads only staged rows: no checks there
-    for (int u0 = 0; u0 < total; u0 += 2 * C) {
-        const int q0 = u0 >> 1;
-        // activity of the rotation's C row pairs, lane j < C testing pair q0 + j: rows 2q, 2q+1
-        // hold a set pixel in columns [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane has
-        // h < C there (exactly the lanes' own test); staged rows past H read as zero
-        uint32_t any = 0u;
-        if (lane < C && q0 + lane < npairs) {
-            const uint2* q = pr + (q0 + lane) * kWinRowWords;
-            const uint2 a = q[0], m = q[1], r = q[2];
-            any = ((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight);
+    int u = 0;
+    if (fast_ok) {
+        // rows y0 = u - C + 1 < 0 are not emitted: rolled steps until the first even u >= C - 1
+        for (; u < ((C - 1 + 1) & ~1) && u < total; u += 2) st.step_rolled(pr + (u >> 1) * kWinRowWords, u, P);
+        // steady state: whole rotations whose emitted rows (up to u + C) all lie in the frame
+        for (; u + C < H; u += 2 * C) {
+            const int q0 = u >> 1;
+            // activity of the rotation's C row pairs, lane j < C testing pair q0 + j: rows 2q,
+            // 2q+1 hold a set pixel in columns [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane
+            // has h < C there (exactly the lanes' own test)
+            uint32_t any = 0u;
+            if (lane < C && q0 + lane < npairs) {
+                const uint2* q = pr + (q0 + lane) * kWinRowWords;
+                const uint2 a = q[0], m = q[1], r = q[2];
+                any = ((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight);
+            }
+            const uint32_t act = __ballot_sync(0xFFFFFFFFu, any != 0u);
+            st.template rotation<0>(pr + q0 * kWinRowWords, act, P);
         }
-        const uint32_t act = __ballot_sync(0xFFFFFFFFu, any != 0u);
-        if (fast_ok && u0 >= 2 * C && u0 + C < H)
-            st.template block<0, true>(pr + q0 * kWinRowWords, act, u0, total, P);
-        else
-            st.template block<0, false>(pr + q0 * kWinRowWords, act, u0, total, P);
     }
+    for (; u < total; u += 2) st.step_rolled(pr + (u >> 1) * kWinRowWords, u, P);
 }
 
 }  // namespace ieds
