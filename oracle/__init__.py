@@ -51,6 +51,8 @@ def _load():
             lib.oracle_surface.argtypes = [P, i64, f64, P]
             lib.oracle_transfer.argtypes = [P, i64, i32, f64, f64, P]
             lib.oracle_quantize_u8.argtypes = [P, i64, P]
+            lib.oracle_quantize_norm_u8.argtypes = [P, i64, i32, f64, P]
+            lib.oracle_quantize_norm_u8.restype = i32
             lib.oracle_window_offsets.argtypes = [P, i64, i64, P, i64]
             lib.oracle_window_offsets.restype = i64
             lib.oracle_alpha_from_dsat.argtypes = [f64]
@@ -150,6 +152,19 @@ def quantize_u8(S) -> np.ndarray:
     S = np.ascontiguousarray(S, dtype=np.float64)
     q = np.empty(S.shape, np.uint8)
     _load().oracle_quantize_u8(_ptr(S), S.size, _ptr(q))
+    return q
+
+
+def quantize_norm_u8(D2, kind: str, bound: float = 6.0) -> np.ndarray:
+    """8-bit view of Id / min(d, bound) / ln(d+1) normalised by the frame maximum:
+    q = round(255 * v / max v); empty frame -> 255, max v = 0 -> 0 (reading R17)."""
+    D2 = np.ascontiguousarray(D2, dtype=np.int64)
+    q = np.empty(D2.shape, np.uint8)
+    rc = _load().oracle_quantize_norm_u8(_ptr(D2), D2.size, TRANSFERS[kind], float(bound), _ptr(q))
+    if rc == -1:
+        raise ValueError("Eq. (1) is coded without normalisation (quantize_u8)")
+    if rc != 0:
+        raise MemoryError("oracle_quantize_norm_u8")
     return q
 
 

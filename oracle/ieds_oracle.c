@@ -284,6 +284,37 @@ void oracle_quantize_u8(const double *S, int64_t n, uint8_t *q)
     }
 }
 
+/* ---- 8-bit view of an ablation transfer, normalised by its frame maximum (row f1):
+ * SPEC S:254 "linear/log variants are first normalized by their frame maximum before
+ * quantization" and S:271 (the paper is silent; reading R17).  For one frame of n pixels:
+ *     v(p) = transfer(D2(p))  (kind 1 Id, 2 min(d, bound), 3 ln(d + 1); as oracle_transfer)
+ *     q(p) = round(255 * v(p) / max_p v(p)), half away from zero, clamped to [0, 255].
+ * Empty frame (every D2 is NO_EDGE): q = 255 everywhere (the saturated state).
+ * max_p v = 0 (every pixel is an edge pixel): q = 0 everywhere (reading R17).
+ * Returns 0, or -1 for kind 0 (Eq. (1) is coded without normalisation, oracle_quantize_u8). */
+int oracle_quantize_norm_u8(const int64_t *D2, int64_t n, int kind, double bound, uint8_t *q)
+{
+    if (kind < 1 || kind > 3) return -1;
+    if (n > 0 && D2[0] == ORACLE_NO_EDGE) {
+        for (int64_t i = 0; i < n; i++) q[i] = 255;
+        return 0;
+    }
+    double *v = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    if (!v) return -2;
+    oracle_transfer(D2, n, kind, 1.0, bound, v);
+    double vmax = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        if (v[i] > vmax) vmax = v[i];
+    for (int64_t i = 0; i < n; i++) {
+        double t = vmax > 0.0 ? floor(255.0 * (v[i] / vmax) + 0.5) : 0.0;
+        if (t < 0.0) t = 0.0;
+        if (t > 255.0) t = 255.0;
+        q[i] = (uint8_t)t;
+    }
+    free(v);
+    return 0;
+}
+
 /* ---- Eq. (2)-(3): alpha = -d_sat / ln(eps), eps = 1/255 --------------------
  * The paper prints alpha ~ d_sat / 5.541, i.e. ln 255 = 5.5413; the oracle keeps
  * the full-precision ln (reading R6).  d_sat <= 0 (or NaN) returns NaN. */

@@ -340,3 +340,28 @@ def test_window_offsets_match_floor_rule():
     for k in range(len(off) - 1):
         assert np.all(k_of[off[k]:off[k + 1]] == k)
     assert off[-1] == len(t)
+
+
+def test_quantize_norm_u8_hand_worked():
+    """8-bit view of the ablation transfers normalised by the frame max (R17).
+    Values worked by hand on frames whose distances are known in closed form."""
+    row = np.array([[0, 1, 4, 9, 16, 25]], np.int64)          # 1x6 row, edge pixel at x = 0
+    # Id: v = x, max 5 -> q = 255 x / 5 = 51 x (exact integers)
+    assert oracle.quantize_norm_u8(row, "linear").tolist() == [[0, 51, 102, 153, 204, 255]]
+    # min(d, 2): v = 0,1,2,2,2,2 -> q(1) = 127.5, rounded half away from zero to 128
+    assert oracle.quantize_norm_u8(row, "bounded", bound=2.0).tolist() == [[0, 128, 255, 255, 255, 255]]
+    # ln(d+1) on x = 0..3: ln 2 / ln 4 = 1/2 exactly -> 128; 255 ln 3 / ln 4 = 202.08 -> 202
+    assert oracle.quantize_norm_u8(row[:, :4], "log").tolist() == [[0, 128, 202, 255]]
+    # 5x5 frame with one edge pixel in the centre: D2 in {0,1,2,4,5,8}, Id normalised by sqrt 8:
+    # 255/sqrt8 = 90.16 -> 90; 255 sqrt2/sqrt8 = 127.5 -> 128; 255*2/sqrt8 = 180.3 -> 180;
+    # 255 sqrt5/sqrt8 = 201.6 -> 202; corners 255
+    yy, xx = np.mgrid[0:5, 0:5]
+    D2 = (yy - 2) ** 2 + (xx - 2) ** 2
+    q = oracle.quantize_norm_u8(D2, "linear")
+    want = {0: 0, 1: 90, 2: 128, 4: 180, 5: 202, 8: 255}
+    assert all(q[i, j] == want[int(D2[i, j])] for i in range(5) for j in range(5))
+    # empty frame -> 255 (S:269); every pixel an edge -> max v = 0 -> 0
+    assert (oracle.quantize_norm_u8(np.full((3, 4), oracle.NO_EDGE), "log") == 255).all()
+    assert (oracle.quantize_norm_u8(np.zeros((3, 4), np.int64), "linear") == 0).all()
+    with pytest.raises(ValueError):
+        oracle.quantize_norm_u8(row, "invexp")
