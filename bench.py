@@ -369,11 +369,10 @@ def run_ours(args):
                  "achieved_gbs": xe_bytes / (xe_avg / 1e3) / 1e9, "frac": xe_bytes / (xe_avg / 1e3) / 1e9 / peak,
                  "note": "IEDS_FLAG_EXACT_EDT: D2 exact everywhere (the kernel sqdist requests use)"}
 
-    # row f1: the same workload with the 8-bit coded surface, 1 B/px written
-    f1 = None
-    if not args.no_f1:
-        Q = torch.empty((nwin, H, W), dtype=torch.uint8, device=dev)
-        bq = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local, out="u8")
+    # row f1: the same workload with the epilogue variants (1 or 2 B/px written)
+    def time_variant(out, transfer, odt, bpp, label, note, kernel_frac=True):
+        Q = torch.empty((nwin, H, W), dtype=odt, device=dev)
+        bq = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local, out=out, transfer=transfer)
         for _ in range(max(1, args.warmup)):
             bq.build_batch(txy, toff, Q)
         torch.cuda.synchronize(dev)
@@ -396,16 +395,28 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(tq, op=dist.ReduceOp.MAX)
         qms = float(tq.item()) / ksteps
-        qe_ms, qe_n = qp["edt"]
-        q_bytes = 1.0 * W * H * (nwin / max(1, qe_n // ksteps))
-        q_gbs = q_bytes / (qe_ms / max(1, qe_n) / 1e3) / 1e9
-        path_q = (4.0 * n_ev + 1.0 * W * H * nwin) / (qms / 1e3) / 1e9
-        f1 = {"variant": "8-bit coded surface q = round(255*S) (P:231)", "value": total_windows / (qms / 1e3),
-              "unit": UNIT, "ms_per_step": qms, "steps": ksteps,
-              "window_kernel_gbs": q_gbs, "window_kernel_frac": q_gbs / peak,
-              "path_gbs": path_q, "path_frac": path_q / peak,
-              "note": "algorithmic bytes 4 B/event + 1 B/px; saturation radius C = 8 (q = 255 from D2 >= 46)"}
+        path_q = (4.0 * n_ev + bpp * W * H * nwin) / (qms / 1e3) / 1e9
+        r = {"variant": label, "value": total_windows / (qms / 1e3), "unit": UNIT, "ms_per_step": qms,
+             "steps": ksteps, "path_gbs": path_q, "path_frac": path_q / peak, "note": note}
+        if kernel_frac:
+            qe_ms, qe_n = qp["edt"]
+            q_bytes = bpp * W * H * (nwin / max(1, qe_n // ksteps))
+            q_gbs = q_bytes / (qe_ms / max(1, qe_n) / 1e3) / 1e9
+            r["window_kernel_gbs"] = q_gbs
+            r["window_kernel_frac"] = q_gbs / peak
         del Q
+        return r
+
+    f1 = f1_f16 = f1_norm = None
+    if not args.no_f1:
+        f1 = time_variant("u8", "invexp", torch.uint8, 1.0, "8-bit coded surface q = round(255*S) (P:231)",
+                          "algorithmic bytes 4 B/event + 1 B/px; saturation radius C = 8 (q = 255 from D2 >= 46)")
+        f1_f16 = time_variant("f16", "invexp", torch.float16, 2.0, "float16 surface (Eq. (1) rounded to nearest even)",
+                              "algorithmic bytes 4 B/event + 2 B/px; saturation radius C = 10 (fp16 1.0 from D2 >= 82)")
+        f1_norm = time_variant("u8", "log", torch.uint8, 1.0,
+                               "8-bit ln(d+1) normalised by the frame maximum (S:254, S:271)",
+                               "exact EDT -> D2 scratch -> per-window max -> quantise (fp64 table); "
+                               "algorithmic bytes 4 B/event + 1 B/px", kernel_frac=False)
 
     # row f2: single-window latency (the paper's real-time mode): one window's
     # events -> surface, (a) events resident on the device, (b) through the host-buffer API
@@ -481,6 +492,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "exact_edt_path": exact,
         "f1_u8_surface": f1,
+        "f1_f16_surface": f1_f16,
+        "f1_u8_normalised_log": f1_norm,
         "f2_latency": lat,
     }
     print(json.dumps(line), flush=True)

@@ -13,8 +13,9 @@
  *   a5  surface S = 1 - exp(-sqrt(D2) / alpha) (Eq. (1)), fp32.
  * A window whose E_df is empty has D2 = IEDS_NO_EDGE everywhere and S = 1 (saturated).
  * Row f1 variants (config.transfer / config.out_format): the ablation transfers of §IV-D
- * (Fig. 4) -- Id(d), min(d, bound), ln(d + 1) -- and the 8-bit coding of the
- * surface, q = round(255 * S) half away from zero.
+ * (Fig. 4) -- Id(d), min(d, bound), ln(d + 1) -- the 8-bit coding of the
+ * surface, q = round(255 * S) half away from zero, the 8-bit view of the ablation
+ * transfers normalised by their frame maximum, and float16 surfaces.
  * alpha may be derived from the saturation distance with ieds_alpha_from_dsat (Eq. (2)-(3),
  * P:228-233).
  *
@@ -25,7 +26,8 @@
  *                   events of window b are events_xy[window_offsets[b] .. window_offsets[b+1]).
  *   window_offsets  int64 [num_windows + 1], offsets[0] >= 0, non-decreasing,
  *                   offsets[num_windows] <= n_events; empty windows are allowed.
- *   surfaces        float32 [num_windows][height][width], row-major (uint8 with IEDS_OUT_U8).
+ *   surfaces        float32 [num_windows][height][width], row-major (uint8 with IEDS_OUT_U8,
+ *                   float16 with IEDS_OUT_F16).
  *   *_bits          uint32 [num_windows][height][ceil(width/32)]: bit (x % 32) of word x/32
  *                   is pixel x (LSB = lowest x); padding bits beyond width are 0.
  *   sqdist          uint32 [num_windows][height][width]: exact D2, IEDS_NO_EDGE if the
@@ -77,7 +79,7 @@ typedef struct {
     int32_t flags;          /* IEDS_FLAG_* bits                                          */
     int32_t transfer;       /* IEDS_TRANSFER_*; 0 = Eq. (1)                             */
     double bound;           /* IEDS_TRANSFER_BOUNDED: upper bound in pixels (> 0) */
-    int32_t out_format;     /* IEDS_OUT_F32 (0) or IEDS_OUT_U8 (1, Eq. (1) only)         */
+    int32_t out_format;     /* IEDS_OUT_F32 (0), IEDS_OUT_U8 (1) or IEDS_OUT_F16 (2)     */
 } ieds_config;
 
 /* transfer of the distance d = sqrt(D2) (pixels); an empty frame is the limit d -> inf */
@@ -86,9 +88,16 @@ typedef struct {
 #define IEDS_TRANSFER_BOUNDED 2 /* min(d, bound); empty -> bound                     */
 #define IEDS_TRANSFER_LOG 3     /* ln(d + 1); empty -> +inf                          */
 #define IEDS_OUT_F32 0          /* float32 surfaces                                          */
-#define IEDS_OUT_U8 1           /* uint8 q = round(255 * S), half away from zero;    */
-                                /* requires IEDS_TRANSFER_INVEXP and q saturating (255) for  */
-                                /* some D2 <= 1024                                            */
+#define IEDS_OUT_U8 1           /* uint8.  Eq. (1): q = round(255 * S), half away from zero  */
+                                /* (P:231); q must saturate (255) for some D2 <= 1024.        */
+                                /* Id / min(d, bound) / ln(d+1): q = round(255 * v / vmax),   */
+                                /* vmax = the frame maximum of v; empty   */
+                                /* frame -> 255, vmax = 0 -> 0 (DESIGN reading R17).  This    */
+                                /* mode runs the exact EDT, a per-window max and a quantise   */
+                                /* pass, with a table of v over every D2 of the frame (fp64). */
+#define IEDS_OUT_F16 2          /* float16 (IEEE binary16) surfaces: the fp64 transfer value  */
+                                /* rounded to nearest even (beyond the table, for Id and ln,  */
+                                /* the fp32 value rounded to nearest even)                    */
 
 /* Always run the uncapped exact-EDT kernel.  By default, when sqdist is not requested and
  * the saturation radius c = ceil(sqrt(K_sat)) is <= 31 pixels, the surface is produced by
@@ -134,7 +143,8 @@ int ieds_window_offsets(ieds_handle *h, const int64_t *t_us, int64_t n, int64_t 
 /* Wait for `stream`, then return (and clear) the latched device error, or IEDS_OK. */
 int ieds_sync(ieds_handle *h, void *stream);
 
-/* Number of kernel launches ieds_build_batch issues for num_windows windows. */
+/* Number of kernel launches ieds_build_batch issues for num_windows windows (2 per chunk:
+ * frame + surface kernel; 4 in the normalised 8-bit mode: + per-window max + quantise). */
 int64_t ieds_launches_per_batch(const ieds_handle *h, int32_t num_windows);
 
 /* Per-kernel device timing (tracing).  While enabled, ieds_build_batch records a CUDA event

@@ -46,7 +46,8 @@ class Builder:
 
     Builder(width, height, n_d, n_f, alpha=None, d_sat=6.0) -- alpha defaults to
     alpha_from_dsat(d_sat).  transfer selects Eq. (1) ("invexp") or a §IV-D ablation ("linear",
-    "bounded" with `bound`, "log"); out="u8" gives the 8-bit coded surface.
+    "bounded" with `bound`, "log"); out="u8" gives the 8-bit coded surface (for the
+    ablations, normalised by the frame maximum), out="f16" float16 surfaces.
     exact_edt=True forces the uncapped exact-EDT kernel even when
     only surfaces are requested (the default streaming kernel gives bit-identical surfaces).  build_batch() enqueues on the current torch stream (or the
     given one) and does not synchronise; sync() reports latched device errors.
@@ -145,7 +146,7 @@ class Builder:
         self._check_dev(events_xy, "events_xy", u32)
         self._check_dev(offsets, "offsets", (torch.int64,))
         B = offsets.numel() - 1
-        odt = torch.uint8 if self.out == "u8" else torch.float32
+        odt = {"u8": torch.uint8, "f16": torch.float16}.get(self.out, torch.float32)
         if out is None:
             out = torch.empty((B, self.height, self.width), dtype=odt, device=self.device)
         self._check_dev(out, "out", (odt,))
@@ -193,7 +194,7 @@ class Builder:
         xy = np.ascontiguousarray(events_xy).view(np.uint32)
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         B = len(off) - 1
-        odt = np.uint8 if self.out == "u8" else np.float32
+        odt = {"u8": np.uint8, "f16": np.float16}.get(self.out, np.float32)
         if out is None:
             out = np.empty((B, self.height, self.width), odt)
         if out.dtype != odt or not out.flags.c_contiguous or out.size < B * self.height * self.width:

@@ -46,7 +46,7 @@ class IedsConfig(ctypes.Structure):
 
 IEDS_FLAG_EXACT_EDT = 1
 TRANSFERS = {"invexp": 0, "linear": 1, "bounded": 2, "log": 3}   # IEDS_TRANSFER_*
-OUT_FORMATS = {"f32": 0, "u8": 1}                                  # IEDS_OUT_*
+OUT_FORMATS = {"f32": 0, "u8": 1, "f16": 2}                         # IEDS_OUT_*
 
 
 class IedsError(RuntimeError):

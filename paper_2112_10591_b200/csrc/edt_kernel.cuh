@@ -14,6 +14,7 @@
 // Surface (Eq. (1)): S = 1 - exp(-sqrt(D2)/alpha) from an fp64-built fp32 table
 // over the integer D2; S is exactly 1.0f from the saturation index K_sat on.
 #pragma once
+#include <cuda_fp16.h>
 #include <cstdint>
 
 namespace ieds {
@@ -24,12 +25,12 @@ struct EdtParams {
     const uint32_t* __restrict__ T;                // [nb][NR][W]
     const unsigned long long* __restrict__ colmask;  // [nb][W]
     int W, H, NR, NS, SEGW;
-    void* __restrict__ S;                           // [nb][H][W] float32, or uint8 if out_u8
+    void* __restrict__ S;                           // [nb][H][W] float32 / uint8 / float16 (out_fmt), or null
     uint32_t* __restrict__ D2;                      // [nb][H][W] or null
     const float* __restrict__ lut;                  // [K_lut]
     int K_lut, K_sat;
     float c_exp;                                    // -log2(e) / alpha
-    int transfer, out_u8;                           // IEDS_TRANSFER_*, IEDS_OUT_U8
+    int transfer, out_fmt;                          // IEDS_TRANSFER_*, IEDS_OUT_*
     float bound, sat_value, empty_value;            // saturated value (D2 >= K_sat), empty frame
 };
 
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(512) edt_kernel(EdtParams p) {
     const size_t plane = (size_t)p.H * W;
     float* Sb = reinterpret_cast<float*>(p.S) + (size_t)b * plane;
     uint8_t* Qb = reinterpret_cast<uint8_t*>(p.S) + (size_t)b * plane;
+    __half* Hb = reinterpret_cast<__half*>(p.S) + (size_t)b * plane;
     uint32_t* Db = p.D2 ? p.D2 + (size_t)b * plane : nullptr;
     for (int s = warp; s < NS; s += nwarps) {
         const int a_s = s * SEGW, b_s = min(W, a_s + SEGW);
@@ -292,8 +294,13 @@ __global__ void __launch_bounds__(512) edt_kernel(EdtParams p) {
                     const int row = 4 * k + (lane >> 3), col = lane & 7;
                     const int y = y0 + row;
                     if (y < p.H && col <= c) {
-                        if (p.out_u8) Qb[(size_t)y * W + xb + col] = (uint8_t)stg[row * 9 + col];
-                        else Sb[(size_t)y * W + xb + col] = stg[row * 9 + col];
+                        if (p.S) {
+                            const size_t o = (size_t)y * W + xb + col;
+                            const float v = stg[row * 9 + col];
+                            if (p.out_fmt == 1) Qb[o] = (uint8_t)v;
+                            else if (p.out_fmt == 2) Hb[o] = __float2half_rn(v);   // table values: exact
+                            else Sb[o] = v;
+                        }
                         if (Db) Db[(size_t)y * W + xb + col] = stgd[row * 9 + col];
                     }
                 }

@@ -4,6 +4,7 @@
 // stream-ordered launches chunk by chunk, the latched device error flag, and the
 // pipelined host-buffer entry point.  Kernels: frame_kernel.cuh (a1-a3), edt_kernel.cuh
 // (a4-a5).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +19,7 @@
 #include "edt_kernel.cuh"
 #include "window_kernel.cuh"
 #include "windowing_kernel.cuh"
+#include "norm_kernel.cuh"
 
 #ifndef IEDS_VERSION_STR
 #define IEDS_VERSION_STR "ieds-b200 0.1 (sm_100a)"
@@ -60,6 +62,10 @@ struct ieds_handle {
     int c_sat;                 // ceil(sqrt(K_sat)): rows/columns a near site can be away
     int c_win;                 // window size of the branch-free kernel (>= c_sat)
     bool streaming;            // saturation-aware window kernel usable (K_sat <= 1024)
+    bool norm_u8;              // 8-bit view of Id / min / ln normalised by the frame maximum
+    uint32_t* D2n = nullptr;   // norm_u8: [chunk][H][W] exact D2 scratch
+    uint32_t* wmax = nullptr;  // norm_u8: [chunk] per-window max D2
+    double* vtab = nullptr;    // norm_u8: [(W-1)^2 + (H-1)^2 + 1] fp64 transfer of every D2
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
     uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
@@ -110,6 +116,7 @@ double transfer_f64(int transfer, double d2, double alpha, double bound) {
 float table_value(const ieds_config& c, double d2) {
     const double v = transfer_f64(c.transfer, d2, c.alpha, c.bound);
     if (c.out_format == IEDS_OUT_U8) return (float)std::min(255.0, std::max(0.0, std::floor(255.0 * v + 0.5)));
+    if (c.out_format == IEDS_OUT_F16) return __half2float(__double2half(v));   // RN-even from fp64
     return (float)v;
 }
 
@@ -117,7 +124,8 @@ float table_value(const ieds_config& c, double d2) {
 float limit_value(const ieds_config& c) {
     switch (c.transfer) {
         case IEDS_TRANSFER_INVEXP: return c.out_format == IEDS_OUT_U8 ? 255.0f : 1.0f;
-        case IEDS_TRANSFER_BOUNDED: return (float)c.bound;
+        case IEDS_TRANSFER_BOUNDED:
+            return c.out_format == IEDS_OUT_F16 ? __half2float(__double2half(c.bound)) : (float)c.bound;
         default: return INFINITY;
     }
 }
@@ -184,9 +192,11 @@ int window_size_for(int c) {
 
 
 template <int C>
-void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, bool u8) {
-    if (u8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, ieds::window_smem_bytes(wp.H), st>>>(wp);
-    else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, ieds::window_smem_bytes(wp.H), st>>>(wp);
+void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt) {
+    const size_t smem = ieds::window_smem_bytes(wp.H);
+    if (fmt == IEDS_OUT_U8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+    else if (fmt == IEDS_OUT_F16) ieds::window_kernel<C, uint16_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+    else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
 }
 
 template <int C>
@@ -195,6 +205,9 @@ cudaError_t window_attr_t(size_t smem) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::window_kernel<C, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ieds::window_kernel<C, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
     return e;
 }
@@ -208,7 +221,7 @@ cudaError_t window_attrs(size_t smem) {
     return e;
 }
 
-void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp, bool u8) {
+void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int u8) {
     switch (C) {
         case 4: launch_window_t<4>(grid, st, wp, u8); break;
         case 6: launch_window_t<6>(grid, st, wp, u8); break;
@@ -225,7 +238,9 @@ void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp,
     }
 }
 
-size_t out_elem_bytes(const ieds_handle* h) { return h->cfg.out_format == IEDS_OUT_U8 ? 1 : 4; }
+size_t out_elem_bytes(const ieds_handle* h) {
+    return h->cfg.out_format == IEDS_OUT_U8 ? 1 : h->cfg.out_format == IEDS_OUT_F16 ? 2 : 4;
+}
 
 int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int64_t n_events, int nb,
                  void* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st) {
@@ -274,7 +289,7 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
         dim3 wgrid((h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps, nb);
         prof_pair(h, 1, &pa, &pb);
         if (pa) cudaEventRecord(pa, st);
-        launch_window(h->c_win, wgrid, st, wp, h->cfg.out_format == IEDS_OUT_U8);
+        launch_window(h->c_win, wgrid, st, wp, h->cfg.out_format);
         if (pb) cudaEventRecord(pb, st);
         cudaError_t e2 = cudaGetLastError();
         return e2 == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
@@ -288,22 +303,31 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     ep.NR = h->NR;
     ep.NS = h->NS;
     ep.SEGW = h->SEGW;
-    ep.S = S;
-    ep.D2 = D2;
+    uint32_t* D2e = (h->norm_u8 && !D2) ? h->D2n : D2;   // the normalised 8-bit view needs D2
+    ep.S = h->norm_u8 ? nullptr : S;
+    ep.D2 = D2e;
     ep.lut = h->lut;
     ep.K_lut = h->K_lut;
     ep.K_sat = h->K_sat;
     ep.c_exp = h->c_exp;
     ep.transfer = h->cfg.transfer;
-    ep.out_u8 = h->cfg.out_format == IEDS_OUT_U8;
+    ep.out_fmt = h->cfg.out_format;
     ep.bound = (float)h->cfg.bound;
     ep.sat_value = limit_value(h->cfg);
     ep.empty_value = limit_value(h->cfg);
     dim3 grid(h->NR, nb);
     prof_pair(h, 1, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
-    ieds::edt_kernel<<<grid, h->NS * 32, D2 ? h->smem_edt_d2 : h->smem_edt, st>>>(ep);
+    ieds::edt_kernel<<<grid, h->NS * 32, D2e ? h->smem_edt_d2 : h->smem_edt, st>>>(ep);
     if (pb) cudaEventRecord(pb, st);
+    if (h->norm_u8) {   // row f1: q = round(255 v(D2) / v(max D2)) per window
+        const int64_t npx = (int64_t)ep.W * ep.H;
+        const dim3 ngrid((unsigned)std::min<int64_t>(64, (npx + ieds::kNormThreads - 1) / ieds::kNormThreads), nb);
+        cudaMemsetAsync(h->wmax, 0, sizeof(uint32_t) * nb, st);
+        ieds::d2max_kernel<<<ngrid, ieds::kNormThreads, 0, st>>>(D2e, npx, h->wmax);
+        ieds::norm_u8_kernel<<<ngrid, ieds::kNormThreads, 0, st>>>(D2e, npx, h->wmax, h->vtab,
+                                                                    static_cast<uint8_t*>(S));
+    }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
 }
@@ -344,9 +368,9 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (cfg->transfer < IEDS_TRANSFER_INVEXP || cfg->transfer > IEDS_TRANSFER_LOG) return IEDS_EINVAL;
     if (cfg->transfer == IEDS_TRANSFER_BOUNDED && !(cfg->bound > 0.0 && std::isfinite(cfg->bound)))
         return IEDS_EINVAL;
-    if (cfg->out_format != IEDS_OUT_F32 && cfg->out_format != IEDS_OUT_U8) return IEDS_EINVAL;
-    if (cfg->out_format == IEDS_OUT_U8 &&
-        (cfg->transfer != IEDS_TRANSFER_INVEXP || saturation_index(*cfg) > kLutMax))
+    if (cfg->out_format < IEDS_OUT_F32 || cfg->out_format > IEDS_OUT_F16) return IEDS_EINVAL;
+    if (cfg->out_format == IEDS_OUT_U8 && cfg->transfer == IEDS_TRANSFER_INVEXP &&
+        saturation_index(*cfg) > kLutMax)
         return IEDS_EINVAL;
 
     ieds_handle* h = new ieds_handle();
@@ -385,7 +409,8 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
         h->c_sat = (int)std::min<int64_t>(cs, 1 << 20);
     }
     h->c_win = window_size_for(std::max(2, h->c_sat));
-    h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) &&
+    h->norm_u8 = cfg->out_format == IEDS_OUT_U8 && cfg->transfer != IEDS_TRANSFER_INVEXP;
+    h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) && !h->norm_u8 &&
                    ieds::window_smem_bytes(H) <= (size_t)kMaxSmem;
 
     // 4 zero words + frame (H + 3 rows), then the column bitmap of the exact path
@@ -404,7 +429,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     // 1000-window batch is one frame launch + one window launch with a single partial tail
     // wave instead of four launch pairs whose last one runs a mostly idle wave.  The host
     // path pipelines copies against kernels at a finer 2-wave grain.
-    h->chunk = cfg->chunk_windows > 0 ? cfg->chunk_windows : 8 * nsm;
+    h->chunk = cfg->chunk_windows > 0 ? cfg->chunk_windows : (h->norm_u8 ? 2 : 8) * nsm;   // norm: D2 scratch
     h->host_chunk = std::min(h->chunk, 2 * nsm);
 
     cudaError_t e;
@@ -416,6 +441,17 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMalloc(&h->dummy, sizeof(uint32_t) * 32 * (size_t)h->chunk);
+    if (e == cudaSuccess && h->norm_u8) {
+        const size_t nv = (size_t)(W - 1) * (W - 1) + (size_t)(H - 1) * (H - 1) + 1;
+        e = cudaMalloc(&h->D2n, sizeof(uint32_t) * (size_t)h->chunk * W * H);
+        if (e == cudaSuccess) e = cudaMalloc(&h->wmax, sizeof(uint32_t) * (size_t)h->chunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->vtab, sizeof(double) * nv);
+        if (e == cudaSuccess) {
+            std::vector<double> v(nv);
+            for (size_t i = 0; i < nv; ++i) v[i] = transfer_f64(cfg->transfer, (double)i, cfg->alpha, cfg->bound);
+            e = cudaMemcpy(h->vtab, v.data(), sizeof(double) * nv, cudaMemcpyHostToDevice);
+        }
+    }
     if (e == cudaSuccess) e = cudaMalloc(&h->colmask, sizeof(unsigned long long) * (size_t)h->chunk * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(h->err, 0, sizeof(int));
@@ -447,6 +483,9 @@ void ieds_destroy(ieds_handle* h) {
     cudaFree(h->T);
     cudaFree(h->Edfs);
     cudaFree(h->dummy);
+    cudaFree(h->D2n);
+    cudaFree(h->wmax);
+    cudaFree(h->vtab);
     cudaFree(h->colmask);
     cudaFree(h->err);
     cudaFree(h->lut);
@@ -484,7 +523,7 @@ int ieds_profile_read(ieds_handle* h, double* frame_ms, int64_t* frame_launches,
 
 int64_t ieds_launches_per_batch(const ieds_handle* h, int32_t num_windows) {
     if (!h || num_windows <= 0) return 0;
-    return 2ll * ((num_windows + h->chunk - 1) / h->chunk);
+    return (h->norm_u8 ? 4ll : 2ll) * ((num_windows + h->chunk - 1) / h->chunk);
 }
 
 int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* window_offsets,

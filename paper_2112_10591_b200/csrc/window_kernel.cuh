@@ -23,6 +23,7 @@
 //                 2C VIADDMNMX.U16x2
 //   emit          2 IMAD extracts + 2 LDS (table) + 2 STG + 2 32-bit pointer adds
 #pragma once
+#include <cuda_fp16.h>
 #include <cstdint>
 #include <type_traits>
 
@@ -36,7 +37,7 @@ constexpr int kWinLutMax = 1024;                  // K_sat bound of the window p
 
 struct WinParams {
     const uint32_t* __restrict__ Edf;   // [nb][H][NW+2], word w of row y at 1 + w, zero guards
-    void* __restrict__ S;               // [nb][H][W] float32 or uint8 (OutT)
+    void* __restrict__ S;               // [nb][H][W] float32, uint8 or float16 bits (OutT)
     const float* __restrict__ lut;      // [K_sat + 1], lut[K_sat] = the saturated value
     uint32_t* __restrict__ dummy;       // [nb][32] sink for the lanes of a ragged strip (x >= W)
     int W, H, NW;
@@ -69,6 +70,9 @@ __device__ __forceinline__ void st_cs_bits(float*, uint64_t addr, uint32_t bits)
 }
 __device__ __forceinline__ void st_cs_bits(uint8_t*, uint64_t addr, uint32_t bits) {
     asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(addr), "r"(bits) : "memory");
+}
+__device__ __forceinline__ void st_cs_bits(uint16_t*, uint64_t addr, uint32_t bits) {   // float16 bits
+    asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(addr), "h"((unsigned short)bits) : "memory");
 }
 
 template <int C, typename OutT>
@@ -208,7 +212,10 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     }
     for (int i = threadIdx.x; i <= p.K_sat; i += blockDim.x) {
         const float f = p.lut[i];
-        lut_s[i] = std::is_same<OutT, uint8_t>::value ? (uint32_t)f : __float_as_uint(f);
+        // the table holds values exactly representable in the output type
+        if constexpr (std::is_same<OutT, uint8_t>::value) lut_s[i] = (uint32_t)f;
+        else if constexpr (std::is_same<OutT, uint16_t>::value) lut_s[i] = __half_as_ushort(__float2half_rn(f));
+        else lut_s[i] = __float_as_uint(f);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();

@@ -57,9 +57,8 @@ def test_create_rejects_bad_config_before_touching_cuda(lib):
         return IedsConfig(w, h_, nd, nf, a, 0, 0, flags, transfer, bound, fmt)
 
     bad = [cfg_(w=0), cfg_(nd=5), cfg_(nf=0), cfg_(a=float("nan")), cfg_(a=-2.0), cfg_(h_=3000),
-           cfg_(flags=8), cfg_(transfer=4), cfg_(transfer=2, bound=0.0), cfg_(fmt=2),
-           cfg_(transfer=1, fmt=1),          # 8-bit coding only for Eq. (1)
-           cfg_(a=50.0, fmt=1)]              # 8-bit saturation beyond the 1024-entry table
+           cfg_(flags=8), cfg_(transfer=4), cfg_(transfer=2, bound=0.0), cfg_(fmt=3), cfg_(fmt=-1),
+           cfg_(a=50.0, fmt=1)]              # 8-bit Eq. (1) saturation beyond the 1024-entry table
     for cfg in bad:
         assert lib.ieds_create(ctypes.byref(cfg), ctypes.byref(h)) == IEDS_EINVAL
         assert not h.value

@@ -126,3 +126,70 @@ def test_window_offsets_match_oracle_and_build():
         bld.window_offsets(torch.from_numpy(bad).to(dev), dt)
         with pytest.raises(ieds.IedsOrderError):
             bld.sync()
+
+
+# ----------------------------------------------------------------------------- row f1: fp16 and normalised 8-bit
+
+def _windows_all():
+    """_windows() plus an all-set frame (every pixel an edge pixel: D2 = 0 everywhere)."""
+    xy, off, W, H = _windows()
+    full = pattern_events(W, H, "all")
+    xy2 = np.concatenate([xy, full]).astype(np.uint32)
+    off2 = np.concatenate([off, [off[-1] + len(full)]]).astype(np.int64)
+    return xy2, off2, W, H
+
+
+@pytest.mark.parametrize("transfer", ["invexp", "linear", "bounded", "log"])
+def test_transfer_variants_f16(transfer):
+    """float16 surfaces: the fp64 transfer value rounded to nearest even (numpy's float16
+    conversion) -- bit for bit from the fp64 table and at saturation; beyond the table (Id
+    and ln only, exact kernel) the fp32 value rounded to fp16, within one fp16 ulp."""
+    xy, off, W, H = _windows()
+    a = oracle.alpha_from_dsat(6.0)
+    S_def, _ = _run(xy, off, W, H, 0, 5, transfer, "f16", with_d2=False)
+    S_exact, D2 = _run(xy, off, W, H, 0, 5, transfer, "f16", with_d2=True)
+    assert S_def.dtype == np.float16
+    for b in range(len(off) - 1):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, 0, 5, a)
+        exp16 = oracle.transfer(ref["D2"], transfer, alpha=a, bound=6.0).astype(np.float16)
+        in_table = (ref["D2"] >= 0) & (ref["D2"] < 1024)
+        for S in (S_def[b], S_exact[b]):
+            same = S.view(np.uint16) == exp16.view(np.uint16)
+            if transfer in ("invexp", "bounded"):
+                assert same.all(), (transfer, b)
+            else:
+                assert same[in_table].all() and np.array_equal(np.isinf(S), np.isinf(exp16)), (transfer, b)
+                fin = np.isfinite(exp16)
+                ulp = np.spacing(np.abs(exp16[fin])).astype(np.float64)
+                assert np.all(np.abs(S[fin].astype(np.float64) - exp16[fin].astype(np.float64)) <= ulp), (transfer, b)
+    if transfer in ("invexp", "bounded"):
+        assert np.array_equal(S_def.view(np.uint16), S_exact.view(np.uint16))
+
+
+@pytest.mark.parametrize("transfer", ["linear", "bounded", "log"])
+def test_u8_normalised_by_frame_max_bit_exact(transfer):
+    """8-bit view of the ablation transfers normalised by the frame maximum (SPEC S:254,
+    S:271, R17): bit-exact against the oracle, including the empty (255) and all-edge (0)
+    frames; identical with and without the D2 output."""
+    xy, off, W, H = _windows_all()
+    a = oracle.alpha_from_dsat(6.0)
+    Q, _ = _run(xy, off, W, H, 0, 5, transfer, "u8", with_d2=False, bound=4.0)
+    Q2, D2 = _run(xy, off, W, H, 0, 5, transfer, "u8", with_d2=True, bound=4.0)
+    assert Q.dtype == np.uint8 and np.array_equal(Q, Q2)
+    for b in range(len(off) - 1):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, 0, 5, a)
+        assert np.array_equal(D2[b].astype(np.int64), np.where(ref["D2"] < 0, 0xFFFFFFFF, ref["D2"]))
+        assert np.array_equal(Q[b], oracle.quantize_norm_u8(ref["D2"], transfer, bound=4.0)), (transfer, b)
+    assert (Q[3] == 255).all()      # the empty window
+    assert (Q[-1] == 0).all()       # every pixel an edge pixel
+
+
+def test_u8_normalised_workload_c3_sampled():
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 70, 3)
+    Q, _ = _run(xy, off, c.width, c.height, wl.n_d, wl.n_f, "log", "u8", with_d2=False)
+    for b in range(3):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a)
+        assert np.array_equal(Q[b], oracle.quantize_norm_u8(ref["D2"], "log")), b
