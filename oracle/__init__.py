@@ -55,6 +55,8 @@ def _load():
             lib.oracle_quantize_norm_u8.restype = i32
             lib.oracle_window_offsets.argtypes = [P, i64, i64, P, i64]
             lib.oracle_window_offsets.restype = i64
+            lib.oracle_fwl.argtypes = [P, P, P, i64, i32, i32, P, i64, i64, P, P, P]
+            lib.oracle_fwl.restype = i32
             lib.oracle_alpha_from_dsat.argtypes = [f64]
             lib.oracle_alpha_from_dsat.restype = f64
             lib.oracle_build_window.argtypes = [P, i64, i32, i32, i32, i32, f64, P, P, P, P, P]
@@ -166,6 +168,30 @@ def quantize_norm_u8(D2, kind: str, bound: float = 6.0) -> np.ndarray:
     if rc != 0:
         raise MemoryError("oracle_quantize_norm_u8")
     return q
+
+
+def fwl(xy, t_us, p, width: int, height: int, flow, t_ref_us: int, dt_us: int, images: bool = False) -> dict:
+    """Row f3: flow-compensated event image and the Flow Warping
+    Loss of one window.  flow is float32 [H][W][2] (dx, dy) in pixels per dt_us.  Returns
+    {"var_comp", "var_uncomp", "fwl"} (+ "I_comp", "I_uncomp" fp64 [H][W] if images)."""
+    xy = np.ascontiguousarray(xy, dtype=np.uint32)
+    t = np.ascontiguousarray(t_us, dtype=np.int64)
+    pp = np.ascontiguousarray(p, dtype=np.int8)
+    F = np.ascontiguousarray(flow, dtype=np.float32)
+    assert F.shape == (height, width, 2) and len(t) == len(xy) == len(pp)
+    out3 = np.empty(3, np.float64)
+    ic = np.empty((height, width), np.float64) if images else None
+    iu = np.empty((height, width), np.float64) if images else None
+    st = _load().oracle_fwl(_ptr(xy), _ptr(t), _ptr(pp), len(xy), width, height, _ptr(F), int(t_ref_us),
+                            int(dt_us), _ptr(ic) if images else None, _ptr(iu) if images else None, _ptr(out3))
+    if st == -1:
+        raise ValueError("invalid parameters")
+    if st == -2:
+        raise OracleRangeError("event outside the frame")
+    r = {"var_comp": float(out3[0]), "var_uncomp": float(out3[1]), "fwl": float(out3[2])}
+    if images:
+        r["I_comp"], r["I_uncomp"] = ic, iu
+    return r
 
 
 def alpha_from_dsat(d_sat: float) -> float:

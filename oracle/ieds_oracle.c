@@ -350,3 +350,77 @@ int oracle_build_window(const uint32_t *xy, int64_t n, int W, int H, int N_d, in
     if (!D2) free(d2);
     return st;
 }
+
+/* ==== Row f3: flow-compensated event image and the Flow Warping Loss ======================
+ * PAPER P:293-297 (FWL of Stoffregen et al.): "compensate and accumulate each raw event
+ * (considering its polarity and timestamp) by its computed optical flow, in order to recreate
+ * an image of compensated events at a reference time t", FWL = sigma^2(I_comp) /
+ * sigma^2(I_uncomp), sigma^2 = the image variance.  SPEC S:393-411 fixes the rest:
+ *   - event (t, x, y, p) carries signed mass +1 (p > 0) or -1 (reading R19: p <= 0 is -1);
+ *   - it is splatted bilinearly at (x, y) + F(x, y) * (t_ref - t) / dt;
+ *   - events landing outside the frame are dropped: reading R19, the warped position
+ *     must lie in [0, W-1] x [0, H-1], so every bilinear corner that receives a non-zero weight
+ *     is a frame pixel;
+ *   - I_uncomp is the same accumulation with zero flow (the plain signed event image);
+ *   - sigma^2 is the population variance over all W*H pixels, two-pass.
+ * F is a dense float32 field [H][W][2] = (dx, dy) in pixels per dt (reading R20).  The warp
+ * arithmetic is fp64 in this order: tau = (t_ref - t) / dt; xw = x + Fx * tau; yw = y + Fy * tau;
+ * x0 = floor(xw), fx = xw - x0 (same for y); weights (1-fx)(1-fy), fx(1-fy), (1-fx)fy, fx fy.
+ * out3 = {var(I_comp), var(I_uncomp), FWL}; FWL is NaN when var(I_uncomp) = 0.
+ * I_comp / I_uncomp may be NULL.  Returns ORACLE_OK, or ORACLE_ERANGE if an event lies
+ * outside the frame (it is dropped, as in oracle_accumulate) / ORACLE_EINVAL. */
+int oracle_fwl(const uint32_t *xy, const int64_t *t, const int8_t *p, int64_t n, int W, int H,
+               const float *flow, int64_t t_ref, int64_t dt, double *I_comp, double *I_uncomp,
+               double *out3)
+{
+    if (W <= 0 || H <= 0 || dt <= 0) return ORACLE_EINVAL;
+    size_t npx = (size_t)W * (size_t)H;
+    double *ic = I_comp ? I_comp : (double *)malloc(sizeof(double) * npx);
+    double *iu = I_uncomp ? I_uncomp : (double *)malloc(sizeof(double) * npx);
+    if (!ic || !iu) return ORACLE_EINVAL;
+    for (size_t i = 0; i < npx; i++) ic[i] = iu[i] = 0.0;
+    int st = ORACLE_OK;
+    for (int64_t e = 0; e < n; e++) {
+        int x = (int)(xy[e] & 0xFFFFu), y = (int)(xy[e] >> 16);
+        if (x >= W || y >= H) {
+            st = ORACLE_ERANGE;
+            continue;
+        }
+        double s = p[e] > 0 ? 1.0 : -1.0;
+        iu[(size_t)y * W + x] += s;
+        double tau = (double)(t_ref - t[e]) / (double)dt;
+        double fxv = (double)flow[((size_t)y * W + x) * 2 + 0];
+        double fyv = (double)flow[((size_t)y * W + x) * 2 + 1];
+        double xw = (double)x + fxv * tau;
+        double yw = (double)y + fyv * tau;
+        if (!(xw >= 0.0 && xw <= (double)(W - 1) && yw >= 0.0 && yw <= (double)(H - 1))) continue;
+        double x0 = floor(xw), y0 = floor(yw);
+        double fx = xw - x0, fy = yw - y0;
+        double ax = 1.0 - fx, ay = 1.0 - fy;
+        int ix = (int)x0, iy = (int)y0;
+        ic[(size_t)iy * W + ix] += s * (ax * ay);
+        if (ix + 1 < W) ic[(size_t)iy * W + ix + 1] += s * (fx * ay);
+        if (iy + 1 < H) ic[(size_t)(iy + 1) * W + ix] += s * (ax * fy);
+        if (ix + 1 < W && iy + 1 < H) ic[(size_t)(iy + 1) * W + ix + 1] += s * (fx * fy);
+    }
+    double mc = 0.0, mu = 0.0;
+    for (size_t i = 0; i < npx; i++) {
+        mc += ic[i];
+        mu += iu[i];
+    }
+    mc /= (double)npx;
+    mu /= (double)npx;
+    double vc = 0.0, vu = 0.0;
+    for (size_t i = 0; i < npx; i++) {
+        vc += (ic[i] - mc) * (ic[i] - mc);
+        vu += (iu[i] - mu) * (iu[i] - mu);
+    }
+    vc /= (double)npx;
+    vu /= (double)npx;
+    out3[0] = vc;
+    out3[1] = vu;
+    out3[2] = vu > 0.0 ? vc / vu : NAN;
+    if (!I_comp) free(ic);
+    if (!I_uncomp) free(iu);
+    return st;
+}

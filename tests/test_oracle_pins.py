@@ -365,3 +365,112 @@ def test_quantize_norm_u8_hand_worked():
     assert (oracle.quantize_norm_u8(np.zeros((3, 4), np.int64), "linear") == 0).all()
     with pytest.raises(ValueError):
         oracle.quantize_norm_u8(row, "invexp")
+
+
+# ---------------------------------------------------------------- row f3: FWL
+
+def _ev(points, W, H, dt=1000):
+    """Hand-built events: list of (x, y, t_us, p)."""
+    a = np.array(points, dtype=np.int64).reshape(-1, 4)
+    xy = (a[:, 0] | (a[:, 1] << 16)).astype(np.uint32)
+    return xy, a[:, 2].astype(np.int64), a[:, 3].astype(np.int8)
+
+
+def test_fwl_hand_worked_splats():
+    W, H, dt = 12, 10, 1000
+    F = np.zeros((H, W, 2), np.float32)
+    # S:400: one event at (5,5) at the window start, t_ref = window end, F(5,5) = (1,0): unit mass at (6,5)
+    xy, t, p = _ev([(5, 5, 0, 1)], W, H)
+    F[5, 5] = (1.0, 0.0)
+    r = oracle.fwl(xy, t, p, W, H, F, dt, dt, images=True)
+    want = np.zeros((H, W)); want[5, 6] = 1.0
+    assert np.array_equal(r["I_comp"], want)
+    u = np.zeros((H, W)); u[5, 5] = 1.0
+    assert np.array_equal(r["I_uncomp"], u)
+    # half-pixel landing (5.5, 5.25): weights 0.5*0.75, 0.5*0.75, 0.5*0.25, 0.5*0.25
+    F[5, 5] = (0.5, 0.25)
+    r = oracle.fwl(xy, t, p, W, H, F, dt, dt, images=True)
+    want = np.zeros((H, W)); want[5, 5] = want[5, 6] = 0.375; want[6, 5] = want[6, 6] = 0.125
+    assert np.array_equal(r["I_comp"], want)
+    # half the window to go (tau = 1/2) with F = (2, 0): lands one pixel right; p = -1 (and p = 0) carry -1
+    F[5, 5] = (2.0, 0.0)
+    for pol in (-1, 0):
+        xy, t, p = _ev([(5, 5, dt // 2, pol)], W, H)
+        r = oracle.fwl(xy, t, p, W, H, F, dt, dt, images=True)
+        want = np.zeros((H, W)); want[5, 6] = -1.0
+        assert np.array_equal(r["I_comp"], want)
+    # landing outside [0, W-1] x [0, H-1] drops the event (S:396); exactly on W-1 keeps it
+    F[:] = 0.0
+    F[0, 0] = (-0.5, 0.0)
+    xy, t, p = _ev([(0, 0, 0, 1), (W - 1, 0, 0, 1)], W, H)
+    r = oracle.fwl(xy, t, p, W, H, F, dt, dt, images=True)
+    want = np.zeros((H, W)); want[0, W - 1] = 1.0
+    assert np.array_equal(r["I_comp"], want)
+    assert r["I_uncomp"][0, 0] == 1.0 and r["I_uncomp"][0, W - 1] == 1.0
+
+
+def test_fwl_variance_closed_forms():
+    dt = 1000
+    # 2x2 frame, one +1 event, zero flow: I = [1,0,0,0], population variance 0.1875, FWL = 1
+    xy, t, p = _ev([(0, 0, 0, 1)], 2, 2)
+    r = oracle.fwl(xy, t, p, 2, 2, np.zeros((2, 2, 2), np.float32), dt, dt)
+    assert r["var_uncomp"] == 0.1875 and r["var_comp"] == 0.1875 and r["fwl"] == 1.0
+    # event B at (1,0) at the window start with F = (-1, 0) lands on event A at (0,0) (tau = 0):
+    # I_comp = [2,0,0,0] (var 0.75), I_uncomp = [1,1,0,0] (var 0.25): FWL = 3
+    F = np.zeros((2, 2, 2), np.float32)
+    F[0, 1] = (-1.0, 0.0)
+    xy, t, p = _ev([(0, 0, dt, 1), (1, 0, 0, 1)], 2, 2)
+    r = oracle.fwl(xy, t, p, 2, 2, F, dt, dt)
+    assert r["var_comp"] == 0.75 and r["var_uncomp"] == 0.25 and r["fwl"] == 3.0
+    # no events: zero uncompensated variance -> undefined (NaN; S:406, S:572)
+    xy, t, p = _ev([], 2, 2)
+    assert np.isnan(oracle.fwl(xy, t, p, 2, 2, F, dt, dt)["fwl"])
+
+
+def test_fwl_invariants_on_generated_scenes():
+    from synth.events import DAVIS
+    from synth.flowscene import affine_flow, flow_field, flow_window
+
+    cfg = DAVIS
+    fl = affine_flow(cfg.width, cfg.height, 1, 0)
+    xy, t, p, t0 = flow_window(cfg, 1, 0, fl)
+    F = flow_field(cfg.width, cfg.height, fl)
+    tref = t0 + cfg.dt_us
+    # zero flow -> exactly 1 (S:408, S:414)
+    r0 = oracle.fwl(xy, t, p, cfg.width, cfg.height, np.zeros_like(F), tref, cfg.dt_us)
+    assert r0["fwl"] == 1.0
+    # the true flow sharpens (S:409: FWL > 1 when the flow is right); scrambled |F| = 10 blurs (S:410)
+    rt = oracle.fwl(xy, t, p, cfg.width, cfg.height, F, tref, cfg.dt_us, images=True)
+    rnd = np.random.default_rng(7).uniform(-10, 10, F.shape).astype(np.float32)
+    rr = oracle.fwl(xy, t, p, cfg.width, cfg.height, rnd, tref, cfg.dt_us)
+    assert rt["fwl"] > 1.05 and rr["fwl"] < 1.0
+    # mass conservation (S:415): with the field scaled so no event can leave the frame from
+    # inside a 10-px margin, the signed mass of the margin-interior events is conserved
+    x, y = xy & 0xFFFF, xy >> 16
+    inner = (x >= 10) & (x < cfg.width - 10) & (y >= 10) & (y < cfg.height - 10)
+    rc = oracle.fwl(xy[inner], t[inner], p[inner], cfg.width, cfg.height, F, tref, cfg.dt_us, images=True)
+    assert abs(rc["I_comp"].sum() - float(np.where(p[inner] > 0, 1, -1).sum())) < 1e-9
+    assert rc["I_uncomp"].sum() == float(np.where(p[inner] > 0, 1, -1).sum())
+
+
+def test_fwl_translating_square_spec_example():
+    """a square outline translating 4 px over the window, compensated by its true flow,
+    gives FWL > 1.05; a random |F| = 10 field gives FWL < 1."""
+    W = H = 48
+    dt = 10000
+    rng = np.random.default_rng(3)
+    side = [(x, 12) for x in range(12, 32)] + [(x, 31) for x in range(12, 32)] + \
+           [(12, y) for y in range(12, 32)] + [(31, y) for y in range(12, 32)]
+    pts = []
+    for (x0, y0) in side:
+        for _ in range(6):
+            tau = rng.random()
+            pts.append((int(np.floor(x0 + 4.0 * tau + 0.5)), y0, int(tau * dt), 1))
+    pts.sort(key=lambda e: e[2])
+    xy, t, p = _ev(pts, W, H)
+    F = np.zeros((H, W, 2), np.float32)
+    F[..., 0] = 4.0
+    r = oracle.fwl(xy, t, p, W, H, F, dt, dt)
+    assert r["fwl"] > 1.05
+    rnd = np.random.default_rng(4).uniform(-10, 10, (H, W, 2)).astype(np.float32)
+    assert oracle.fwl(xy, t, p, W, H, rnd, dt, dt)["fwl"] < 1.0
