@@ -140,6 +140,30 @@ int ieds_build_batch_host(ieds_handle *h, const uint32_t *events_xy,
 int ieds_window_offsets(ieds_handle *h, const int64_t *t_us, int64_t n, int64_t t0_us, int64_t dt_us,
                         int32_t num_windows, int64_t *window_offsets, void *stream);
 
+/* Row f3: flow-compensated event image and Flow Warping Loss of each window (PAPER P:293-297,
+ * FWL = var(I_comp) / var(I_uncomp)).  For window b (events
+ * window_offsets[b] .. window_offsets[b+1] of the device arrays):
+ *   I_uncomp  = signed event image: +1 for events_p > 0, -1 otherwise, at (x, y);
+ *   I_comp    = each event's signed unit mass splatted bilinearly at
+ *               (x, y) + F_b(x, y) * (t_ref_us[b] - t) / dt_us, evaluated in fp64; an event whose
+ *               warped position lies outside [0, W-1] x [0, H-1] is dropped (DESIGN R19);
+ *   var       = population variance over all W*H pixels; fwl[b] = var(I_comp) / var(I_uncomp),
+ *               NaN when var(I_uncomp) = 0 (no events).
+ * Arguments (DEVICE pointers): events_xy uint32 [n_events] (x | y << 16), events_t_us int64
+ * [n_events], events_p int8 [n_events], window_offsets int64 [num_windows + 1] (as in
+ * ieds_build_batch), flow float32 [num_windows][H][W][2] = (dx, dy) pixels per dt_us (dense,
+ * DESIGN R20), t_ref_us int64 [num_windows] (SPEC: the window end), dt_us > 0.
+ * Outputs: fwl double [num_windows] (required); var_comp, var_uncomp double [num_windows] and
+ * comp_image double [num_windows][H][W] (I_comp) are optional (NULL to skip).
+ * Out-of-frame events latch IEDS_ERANGE and are dropped; bad offsets latch IEDS_EORDER (both
+ * reported by ieds_sync).  The handle allocates its f3 scratch (8 windows of fp64 + int32
+ * images) on the first call.  Enqueued on `stream`; returns IEDS_EINVAL for bad arguments. */
+int ieds_fwl_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *events_t_us,
+                   const int8_t *events_p, const int64_t *window_offsets, int64_t n_events,
+                   int32_t num_windows, const float *flow, const int64_t *t_ref_us, int64_t dt_us,
+                   double *fwl, double *var_comp, double *var_uncomp, double *comp_image,
+                   void *stream);
+
 /* Wait for `stream`, then return (and clear) the latched device error, or IEDS_OK. */
 int ieds_sync(ieds_handle *h, void *stream);
 

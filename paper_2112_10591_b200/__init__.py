@@ -182,6 +182,40 @@ class Builder:
                                          self._stream(stream)), "ieds_window_offsets")
         return off
 
+    def fwl_batch(self, events_xy, events_t_us, events_p, offsets, flow, t_ref_us, dt_us: int, *,
+                  variances: bool = False, comp_image: bool = False, stream=None) -> dict:
+        """Row f3 (ieds_fwl_batch): Flow Warping Loss of each window.
+        events_xy int32/uint32 [n], events_t_us int64 [n], events_p int8 [n], offsets int64
+        [B+1], flow float32 [B, H, W, 2] (pixels per dt_us), t_ref_us int64 [B] -- all on this
+        device.  Returns {"fwl": float64 [B]} plus "var_comp"/"var_uncomp" [B] and "comp_image"
+        float64 [B, H, W] when asked.  Enqueued; call sync() to surface latched errors."""
+        import torch
+
+        self._check_dev(events_xy, "events_xy", (torch.int32, torch.uint32))
+        self._check_dev(events_t_us, "events_t_us", (torch.int64,))
+        self._check_dev(events_p, "events_p", (torch.int8,))
+        self._check_dev(offsets, "offsets", (torch.int64,))
+        self._check_dev(flow, "flow", (torch.float32,))
+        self._check_dev(t_ref_us, "t_ref_us", (torch.int64,))
+        B = offsets.numel() - 1
+        n = events_xy.numel()
+        if events_t_us.numel() != n or events_p.numel() != n:
+            raise ValueError("events_xy, events_t_us and events_p must have the same length")
+        if tuple(flow.shape) != (B, self.height, self.width, 2) or t_ref_us.numel() != B:
+            raise ValueError("flow must be [B, H, W, 2] and t_ref_us [B]")
+        dev = self.device
+        out = {"fwl": torch.empty(B, dtype=torch.float64, device=dev)}
+        if variances:
+            out["var_comp"] = torch.empty(B, dtype=torch.float64, device=dev)
+            out["var_uncomp"] = torch.empty(B, dtype=torch.float64, device=dev)
+        if comp_image:
+            out["comp_image"] = torch.empty((B, self.height, self.width), dtype=torch.float64, device=dev)
+        check(load().ieds_fwl_batch(self._h, _ptr(events_xy), _ptr(events_t_us), _ptr(events_p), _ptr(offsets), n, B,
+                                    _ptr(flow), _ptr(t_ref_us), int(dt_us), _ptr(out["fwl"]),
+                                    _ptr(out.get("var_comp")), _ptr(out.get("var_uncomp")),
+                                    _ptr(out.get("comp_image")), self._stream(stream)), "ieds_fwl_batch")
+        return out
+
     def sync(self, stream=None):
         """Wait for the stream; raise IedsRangeError / IedsOrderError on latched data errors."""
         check(load().ieds_sync(self._h, self._stream(stream)), "ieds_sync")

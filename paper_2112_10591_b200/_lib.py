@@ -24,7 +24,7 @@ IEDS_NO_EDGE = 0xFFFFFFFF
 # every symbol include/ieds.h declares
 EXPORTS = (
     "ieds_create", "ieds_destroy", "ieds_build_batch", "ieds_build_batch_host", "ieds_sync",
-    "ieds_window_offsets", "ieds_launches_per_batch", "ieds_profile_enable", "ieds_profile_read", "ieds_strerror", "ieds_alpha_from_dsat", "ieds_version",
+    "ieds_window_offsets", "ieds_fwl_batch", "ieds_launches_per_batch", "ieds_profile_enable", "ieds_profile_read", "ieds_strerror", "ieds_alpha_from_dsat", "ieds_version",
 )
 
 
@@ -87,6 +87,8 @@ def load():
     lib.ieds_build_batch_host.restype = ctypes.c_int
     lib.ieds_window_offsets.argtypes = [P, P, i64, i64, i64, i32, P, P]
     lib.ieds_window_offsets.restype = ctypes.c_int
+    lib.ieds_fwl_batch.argtypes = [P, P, P, P, P, i64, i32, P, P, i64, P, P, P, P, P]
+    lib.ieds_fwl_batch.restype = ctypes.c_int
     lib.ieds_sync.argtypes = [P, P]
     lib.ieds_sync.restype = ctypes.c_int
     lib.ieds_launches_per_batch.argtypes = [P, i32]

@@ -20,6 +20,7 @@
 #include "window_kernel.cuh"
 #include "windowing_kernel.cuh"
 #include "norm_kernel.cuh"
+#include "fwl_kernel.cuh"
 
 #ifndef IEDS_VERSION_STR
 #define IEDS_VERSION_STR "ieds-b200 0.1 (sm_100a)"
@@ -30,7 +31,8 @@ namespace {
 constexpr int kFrameThreads = 1024;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
 constexpr int kLutMax = ieds::kWinLutMax;
-constexpr int kSegTarget = 80;     // columns per EDT segment (warp)
+constexpr int kSegTarget = 80;
+constexpr int kFwlChunk = 8;       // row f3: windows per splat/reduce pass (12 B/px of L2 scratch each)     // columns per EDT segment (warp)
 
 struct HostPath {
     cudaStream_t st[2] = {nullptr, nullptr};
@@ -66,6 +68,11 @@ struct ieds_handle {
     uint32_t* D2n = nullptr;   // norm_u8: [chunk][H][W] exact D2 scratch
     uint32_t* wmax = nullptr;  // norm_u8: [chunk] per-window max D2
     double* vtab = nullptr;    // norm_u8: [(W-1)^2 + (H-1)^2 + 1] fp64 transfer of every D2
+    // row f3 scratch (allocated on the first ieds_fwl_batch): kFwlChunk windows of images
+    double* fwl_Ic = nullptr;             // [kFwlChunk][H][W] fp64, zero between calls
+    int* fwl_Iu = nullptr;                // [kFwlChunk][H][W] int32, zero between calls
+    double* fwl_acc = nullptr;            // [kFwlChunk][2]
+    unsigned long long* fwl_accu = nullptr;
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
     uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
@@ -484,6 +491,10 @@ void ieds_destroy(ieds_handle* h) {
     cudaFree(h->Edfs);
     cudaFree(h->dummy);
     cudaFree(h->D2n);
+    cudaFree(h->fwl_Ic);
+    cudaFree(h->fwl_Iu);
+    cudaFree(h->fwl_acc);
+    cudaFree(h->fwl_accu);
     cudaFree(h->wmax);
     cudaFree(h->vtab);
     cudaFree(h->colmask);
@@ -577,6 +588,72 @@ int ieds_sync(ieds_handle* h, void* stream) {
     if (f & ieds::kErrOrder) return IEDS_EORDER;
     if (f & ieds::kErrRange) return IEDS_ERANGE;
     return IEDS_OK;
+}
+
+int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* events_t_us, const int8_t* events_p,
+                   const int64_t* window_offsets, int64_t n_events, int32_t num_windows, const float* flow,
+                   const int64_t* t_ref_us, int64_t dt_us, double* fwl, double* var_comp, double* var_uncomp,
+                   double* comp_image, void* stream) {
+    if (!h || num_windows < 0 || n_events < 0 || dt_us <= 0) return IEDS_EINVAL;
+    if (num_windows == 0) return IEDS_OK;
+    if (!window_offsets || !flow || !t_ref_us || !fwl) return IEDS_EINVAL;
+    if (n_events > 0 && (!events_xy || !events_t_us || !events_p)) return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    const int W = h->cfg.width, H = h->cfg.height;
+    const int64_t npx = (int64_t)W * H;
+    cudaError_t e = cudaSuccess;
+    if (!h->fwl_Ic) {
+        e = cudaMalloc(&h->fwl_Ic, sizeof(double) * npx * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * npx * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_acc, sizeof(double) * 2 * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_accu, sizeof(unsigned long long) * 2 * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMemset(h->fwl_Ic, 0, sizeof(double) * npx * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMemset(h->fwl_Iu, 0, sizeof(int) * npx * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMemset(h->fwl_acc, 0, sizeof(double) * 2 * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMemset(h->fwl_accu, 0, sizeof(unsigned long long) * 2 * kFwlChunk);
+        if (e != cudaSuccess) {
+            cudaFree(h->fwl_Ic);
+            cudaFree(h->fwl_Iu);
+            cudaFree(h->fwl_acc);
+            cudaFree(h->fwl_accu);
+            h->fwl_Ic = nullptr;
+            h->fwl_Iu = nullptr;
+            h->fwl_acc = nullptr;
+            h->fwl_accu = nullptr;
+            cudaGetLastError();
+            return cuda_fail(e);
+        }
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // splat grid: enough blocks per window to fill the GPU several times over
+    const int per_win = std::max(1, (4 * 148) / kFwlChunk);
+    const int red_blocks = (int)std::min<int64_t>(64, (npx + ieds::kFwlThreads - 1) / ieds::kFwlThreads);
+    for (int c0 = 0; c0 < num_windows; c0 += kFwlChunk) {
+        const int nb = std::min(kFwlChunk, num_windows - c0);
+        ieds::FwlParams fp;
+        fp.xy = events_xy;
+        fp.t = events_t_us;
+        fp.p = events_p;
+        fp.offsets = window_offsets + c0;
+        fp.n_events = n_events;
+        fp.flow = reinterpret_cast<const float2*>(flow) + (size_t)c0 * npx;
+        fp.t_ref = t_ref_us + c0;
+        fp.dt = dt_us;
+        fp.W = W;
+        fp.H = H;
+        fp.Ic = h->fwl_Ic;
+        fp.Iu = h->fwl_Iu;
+        fp.err = h->err;
+        ieds::fwl_splat_kernel<<<dim3(per_win, nb), ieds::kFwlThreads, 0, st>>>(fp);
+        ieds::fwl_reduce_kernel<<<dim3(red_blocks, nb), ieds::kFwlThreads, 0, st>>>(
+            h->fwl_Ic, h->fwl_Iu, npx, h->fwl_acc, h->fwl_accu, comp_image ? comp_image + (size_t)c0 * npx : nullptr);
+        ieds::fwl_finalize_kernel<<<1, 32, 0, st>>>(h->fwl_acc, h->fwl_accu, npx, nb, fwl + c0,
+                                                     var_comp ? var_comp + c0 : nullptr,
+                                                     var_uncomp ? var_uncomp + c0 : nullptr);
+    }
+    e = cudaGetLastError();
+    return e == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
 }
 
 int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64_t* window_offsets,
