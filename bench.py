@@ -236,6 +236,73 @@ def run_reference(args):
     return 0
 
 
+def run_f3(args, dev, stream, world, local, peak):
+    """Row f3: ieds_fwl_batch over C3-geometry windows of a scene moving under a known dense
+    affine flow (synth/flowscene.py), inputs resident on the device.  Algorithmic bytes per
+    event: 4 (xy) + 8 (t) + 1 (p) + 8 (the flow gathered at the event pixel)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_10591_b200 as ieds
+    from synth.flowscene import F3_SCENE, flow_batch
+
+    cfg = F3_SCENE
+    nwin = max(1, args.f3_windows)
+    rank = int(os.environ.get("RANK", "0"))
+    xy, t, p, off, flows, _fl, t_ref = flow_batch(cfg, 3, rank * nwin, nwin)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    txy, tt, tp, toff = T(xy.view(np.int32)), T(t), T(p), T(off)
+    tflow, tref = T(flows), T(t_ref)
+    del flows
+    bld = ieds.Builder(cfg.width, cfg.height, 1, 4, device=local)
+    for _ in range(max(1, args.warmup)):
+        r = bld.fwl_batch(txy, tt, tp, toff, tflow, tref, cfg.dt_us)
+    bld.sync()
+    ksteps = max(1, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ksteps):
+        r = bld.fwl_batch(txy, tt, tp, toff, tflow, tref, cfg.dt_us)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    bld.sync()
+    fwl_mean = float(r["fwl"].mean().item())
+    bld.close()
+    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item()) / ksteps
+    n_ev = int(off[-1])
+    bytes_alg = 21.0 * n_ev + 8.0 * (nwin + 1) + 16.0 * nwin
+    out = {"metric": "FWL windows/s (flow-compensated event image + variance ratio, P:293-297)",
+           "value": nwin * max(1, world) / (ms / 1e3), "unit": "windows/s", "ms_per_step": ms, "steps": ksteps,
+           "windows": nwin, "mev_per_s": n_ev * max(1, world) / (ms / 1e3) / 1e6,
+           "hbm_gbs": bytes_alg / (ms / 1e3) / 1e9, "hbm_frac": bytes_alg / (ms / 1e3) / 1e9 / peak,
+           "fwl_mean": fwl_mean,
+           "note": "algorithmic bytes 21 B/event (xy, t, p, flow gather); the I_comp/I_uncomp images are "
+                   "L2-resident scratch (12 B/px, 8 windows per pass), so the bound is L2 atomics + the "
+                   "image reduce, not HBM"}
+    if rank == 0 and not args.no_cpu_baseline:
+        import time as _time
+
+        import oracle
+
+        t0 = _time.perf_counter()
+        nsamp = min(4, nwin)
+        for b in range(nsamp):
+            sl = slice(off[b], off[b + 1])
+            oracle.fwl(xy[sl], t[sl], p[sl], cfg.width, cfg.height,
+                       flow_batch(cfg, 3, rank * nwin + b, 1)[4][0], t_ref[b], cfg.dt_us)
+        dt_o = _time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": nsamp / dt_o, "unit": "windows/s", "cores": 1, "kind": "oracle",
+                               "sample": f"{nsamp} windows, one core, C oracle fp64 (incl. regenerating each field)"}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -418,6 +485,11 @@ def run_ours(args):
                                "exact EDT -> D2 scratch -> per-window max -> quantise (fp64 table); "
                                "algorithmic bytes 4 B/event + 1 B/px", kernel_frac=False)
 
+    # row f3: flow-compensated event image + FWL on C3-geometry moving scenes
+    f3 = None
+    if not args.no_f3:
+        f3 = run_f3(args, dev, stream, world, local, peak)
+
     # row f2: single-window latency (the paper's real-time mode): one window's
     # events -> surface, (a) events resident on the device, (b) through the host-buffer API
     lat = None
@@ -495,6 +567,7 @@ def run_ours(args):
         "f1_f16_surface": f1_f16,
         "f1_u8_normalised_log": f1_norm,
         "f2_latency": lat,
+        "f3_fwl": f3,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -514,6 +587,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-EDT comparison run")
     ap.add_argument("--no-f1", action="store_true", help="skip the 8-bit surface (row f1) run")
+    ap.add_argument("--no-f3", action="store_true", help="skip the FWL (row f3) run")
+    ap.add_argument("--f3-windows", type=int, default=64, help="C3-geometry windows of the FWL (row f3) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")
     ap.add_argument("--cpu-windows", type=int, default=256,

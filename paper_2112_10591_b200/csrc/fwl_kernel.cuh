@@ -29,8 +29,9 @@ struct FwlParams {
     const int64_t* __restrict__ t_ref;     // [nb] reference times (microseconds)
     int64_t dt;                            // microseconds, > 0
     int W, H;
-    double* __restrict__ Ic;               // [nb][H][W] scratch, zero on entry
-    int* __restrict__ Iu;                  // [nb][H][W] scratch, zero on entry
+    int64_t stride;                        // pixels per window image in the scratch (>= W*H, % 4 == 0)
+    double* __restrict__ Ic;               // [nb][stride] scratch, zero on entry
+    int* __restrict__ Iu;                  // [nb][stride] scratch, zero on entry
     int* __restrict__ err;
 };
 
@@ -43,8 +44,8 @@ __global__ void __launch_bounds__(kFwlThreads) fwl_splat_kernel(FwlParams p) {
     }
     const int W = p.W, H = p.H;
     const size_t npx = (size_t)W * H;
-    double* Ic = p.Ic + (size_t)b * npx;
-    int* Iu = p.Iu + (size_t)b * npx;
+    double* Ic = p.Ic + (size_t)b * p.stride;
+    int* Iu = p.Iu + (size_t)b * p.stride;
     const float2* F = p.flow + (size_t)b * npx;
     const int64_t tref = p.t_ref[b];
     const double dt = (double)p.dt, xmax = (double)(W - 1), ymax = (double)(H - 1);
@@ -81,28 +82,54 @@ __global__ void __launch_bounds__(kFwlThreads) fwl_splat_kernel(FwlParams p) {
     if (bad) atomicOr(p.err, 1);   // kErrRange: dropped, latched
 }
 
-// per-window sums of I_comp, I_comp^2 (fp64) and I_uncomp, I_uncomp^2 (exact int64); copies
-// I_comp out if asked; re-zeroes both images.  acc[b] = {sum c, sum c^2}, accu[b] = {sum u, sum u^2}
+// Per-window partial sums of I_comp, I_comp^2 (fp64) and I_uncomp, I_uncomp^2 (exact int64),
+// one partial per block: part[b][blk] = {sum c, sum c^2, sum u, sum u^2}; re-zeroes both
+// images.  Each window's scratch image has a stride that is a multiple of 4 pixels (the pad
+// stays zero), so a thread takes 4 pixels with two 16-byte fp64 loads and one 16-byte int32
+// load, all in flight at once.  With comp_out (tests), a plain per-pixel loop also copies
+// I_comp out.
+struct FwlPart {
+    double c, c2;
+    long long u, u2;
+};
+
 __global__ void __launch_bounds__(kFwlThreads) fwl_reduce_kernel(double* __restrict__ Ic, int* __restrict__ Iu,
-                                                                  int64_t npx, double* __restrict__ acc,
-                                                                  unsigned long long* __restrict__ accu,
+                                                                  int64_t npx, int64_t stride,
+                                                                  FwlPart* __restrict__ part, int nblk,
                                                                   double* __restrict__ comp_out) {
     const int b = blockIdx.y;
-    double* c = Ic + (size_t)b * npx;
-    int* u = Iu + (size_t)b * npx;
-    double* co = comp_out ? comp_out + (size_t)b * npx : nullptr;
+    double* c = Ic + (size_t)b * stride;
+    int* u = Iu + (size_t)b * stride;
     double sc = 0.0, sc2 = 0.0;
     long long su = 0, su2 = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
-        const double cv = c[i];
-        const long long uv = u[i];
-        sc += cv;
-        sc2 = fma(cv, cv, sc2);
-        su += uv;
-        su2 += uv * uv;
-        if (co) co[i] = cv;
-        c[i] = 0.0;
-        u[i] = 0;
+    if (comp_out) {
+        double* co = comp_out + (size_t)b * npx;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
+            const double cv = c[i];
+            const long long uv = u[i];
+            sc += cv;
+            sc2 = fma(cv, cv, sc2);
+            su += uv;
+            su2 += uv * uv;
+            co[i] = cv;
+            c[i] = 0.0;
+            u[i] = 0;
+        }
+    } else {
+        double2* c2 = reinterpret_cast<double2*>(c);
+        int4* u4 = reinterpret_cast<int4*>(u);
+        const int64_t n4 = stride >> 2;
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+            const double2 a = __ldcg(c2 + 2 * j), d = __ldcg(c2 + 2 * j + 1);
+            const int4 w = __ldcg(u4 + j);
+            sc += (a.x + a.y) + (d.x + d.y);
+            sc2 = fma(a.x, a.x, fma(a.y, a.y, fma(d.x, d.x, fma(d.y, d.y, sc2))));
+            su += (long long)w.x + w.y + w.z + w.w;
+            su2 += (long long)w.x * w.x + (long long)w.y * w.y + (long long)w.z * w.z + (long long)w.w * w.w;
+            c2[2 * j] = make_double2(0.0, 0.0);
+            c2[2 * j + 1] = make_double2(0.0, 0.0);
+            u4[j] = make_int4(0, 0, 0, 0);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         sc += __shfl_xor_sync(0xFFFFFFFFu, sc, o);
@@ -110,47 +137,63 @@ __global__ void __launch_bounds__(kFwlThreads) fwl_reduce_kernel(double* __restr
         su += __shfl_xor_sync(0xFFFFFFFFu, su, o);
         su2 += __shfl_xor_sync(0xFFFFFFFFu, su2, o);
     }
-    __shared__ double s_c[kFwlThreads / 32], s_c2[kFwlThreads / 32];
-    __shared__ long long s_u[kFwlThreads / 32], s_u2[kFwlThreads / 32];
+    __shared__ FwlPart s_p[kFwlThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        s_c[warp] = sc;
-        s_c2[warp] = sc2;
-        s_u[warp] = su;
-        s_u2[warp] = su2;
-    }
+    if (lane == 0) s_p[warp] = FwlPart{sc, sc2, su, su2};
     __syncthreads();
     if (threadIdx.x == 0) {
+        FwlPart t = s_p[0];
         for (int k = 1; k < kFwlThreads / 32; ++k) {
-            sc += s_c[k];
-            sc2 += s_c2[k];
-            su += s_u[k];
-            su2 += s_u2[k];
+            t.c += s_p[k].c;
+            t.c2 += s_p[k].c2;
+            t.u += s_p[k].u;
+            t.u2 += s_p[k].u2;
         }
-        atomicAdd(acc + 2 * b, sc);
-        atomicAdd(acc + 2 * b + 1, sc2);
-        atomicAdd(accu + 2 * b, (unsigned long long)su);   // two's complement sum
-        atomicAdd(accu + 2 * b + 1, (unsigned long long)su2);
+        part[(size_t)b * nblk + blockIdx.x] = t;
     }
 }
 
-// var = E[I^2] - E[I]^2 per window; FWL = var_c / var_u (NaN if var_u = 0); re-zeroes acc
-__global__ void fwl_finalize_kernel(double* __restrict__ acc, unsigned long long* __restrict__ accu, int64_t npx,
-                                    int nb, double* __restrict__ fwl, double* __restrict__ var_c,
-                                    double* __restrict__ var_u) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
+// One block per window: sums the partials (fixed order), var = E[I^2] - E[I]^2,
+// FWL = var_c / var_u (NaN if var_u = 0)
+__global__ void __launch_bounds__(kFwlThreads) fwl_finalize_kernel(const FwlPart* __restrict__ part, int nblk,
+                                                                    int64_t npx, double* __restrict__ fwl,
+                                                                    double* __restrict__ var_c,
+                                                                    double* __restrict__ var_u) {
+    const int b = blockIdx.x;
+    double sc = 0.0, sc2 = 0.0;
+    long long su = 0, su2 = 0;
+    for (int k = threadIdx.x; k < nblk; k += blockDim.x) {
+        const FwlPart t = part[(size_t)b * nblk + k];
+        sc += t.c;
+        sc2 += t.c2;
+        su += t.u;
+        su2 += t.u2;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sc += __shfl_xor_sync(0xFFFFFFFFu, sc, o);
+        sc2 += __shfl_xor_sync(0xFFFFFFFFu, sc2, o);
+        su += __shfl_xor_sync(0xFFFFFFFFu, su, o);
+        su2 += __shfl_xor_sync(0xFFFFFFFFu, su2, o);
+    }
+    __shared__ FwlPart s_p[kFwlThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_p[warp] = FwlPart{sc, sc2, su, su2};
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int k = 1; k < (int)(blockDim.x / 32); ++k) {
+        sc += s_p[k].c;
+        sc2 += s_p[k].c2;
+        su += s_p[k].u;
+        su2 += s_p[k].u2;
+    }
     const double N = (double)npx;
-    const double mc = acc[2 * b] / N;
-    const double vc = fmax(acc[2 * b + 1] / N - mc * mc, 0.0);
-    const long long su = (long long)accu[2 * b], su2 = (long long)accu[2 * b + 1];
+    const double mc = sc / N;
+    const double vc = fmax(sc2 / N - mc * mc, 0.0);
     // N * sum u^2 - (sum u)^2 is an exact integer (|sum u| <= n_events)
     const double vu = (double)(npx * su2 - su * su) / (N * N);
     fwl[b] = vu > 0.0 ? vc / vu : __longlong_as_double(0x7FF8000000000000LL);
     if (var_c) var_c[b] = vc;
     if (var_u) var_u[b] = vu;
-    acc[2 * b] = acc[2 * b + 1] = 0.0;
-    accu[2 * b] = accu[2 * b + 1] = 0ull;
 }
 
 }  // namespace ieds

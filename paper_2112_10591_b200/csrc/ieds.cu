@@ -71,8 +71,7 @@ struct ieds_handle {
     // row f3 scratch (allocated on the first ieds_fwl_batch): kFwlChunk windows of images
     double* fwl_Ic = nullptr;             // [kFwlChunk][H][W] fp64, zero between calls
     int* fwl_Iu = nullptr;                // [kFwlChunk][H][W] int32, zero between calls
-    double* fwl_acc = nullptr;            // [kFwlChunk][2]
-    unsigned long long* fwl_accu = nullptr;
+    ieds::FwlPart* fwl_part = nullptr;    // [kFwlChunk][reduce blocks] per-block partial sums
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
     uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
@@ -493,8 +492,7 @@ void ieds_destroy(ieds_handle* h) {
     cudaFree(h->D2n);
     cudaFree(h->fwl_Ic);
     cudaFree(h->fwl_Iu);
-    cudaFree(h->fwl_acc);
-    cudaFree(h->fwl_accu);
+    cudaFree(h->fwl_part);
     cudaFree(h->wmax);
     cudaFree(h->vtab);
     cudaFree(h->colmask);
@@ -602,25 +600,22 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     if (!g.ok) return IEDS_ECUDA;
     const int W = h->cfg.width, H = h->cfg.height;
     const int64_t npx = (int64_t)W * H;
+    const int64_t stride = (npx + 3) & ~3ll;   // 16-byte aligned window images in the scratch
+    const int red_blocks = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (stride / 4 + ieds::kFwlThreads - 1) / ieds::kFwlThreads));
     cudaError_t e = cudaSuccess;
     if (!h->fwl_Ic) {
-        e = cudaMalloc(&h->fwl_Ic, sizeof(double) * npx * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * npx * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_acc, sizeof(double) * 2 * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_accu, sizeof(unsigned long long) * 2 * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMemset(h->fwl_Ic, 0, sizeof(double) * npx * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMemset(h->fwl_Iu, 0, sizeof(int) * npx * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMemset(h->fwl_acc, 0, sizeof(double) * 2 * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMemset(h->fwl_accu, 0, sizeof(unsigned long long) * 2 * kFwlChunk);
+        e = cudaMalloc(&h->fwl_Ic, sizeof(double) * stride * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * stride * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * red_blocks * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMemset(h->fwl_Ic, 0, sizeof(double) * stride * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMemset(h->fwl_Iu, 0, sizeof(int) * stride * kFwlChunk);
         if (e != cudaSuccess) {
             cudaFree(h->fwl_Ic);
             cudaFree(h->fwl_Iu);
-            cudaFree(h->fwl_acc);
-            cudaFree(h->fwl_accu);
+            cudaFree(h->fwl_part);
             h->fwl_Ic = nullptr;
             h->fwl_Iu = nullptr;
-            h->fwl_acc = nullptr;
-            h->fwl_accu = nullptr;
+            h->fwl_part = nullptr;
             cudaGetLastError();
             return cuda_fail(e);
         }
@@ -628,7 +623,6 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // splat grid: enough blocks per window to fill the GPU several times over
     const int per_win = std::max(1, (4 * 148) / kFwlChunk);
-    const int red_blocks = (int)std::min<int64_t>(64, (npx + ieds::kFwlThreads - 1) / ieds::kFwlThreads);
     for (int c0 = 0; c0 < num_windows; c0 += kFwlChunk) {
         const int nb = std::min(kFwlChunk, num_windows - c0);
         ieds::FwlParams fp;
@@ -642,15 +636,17 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
         fp.dt = dt_us;
         fp.W = W;
         fp.H = H;
+        fp.stride = stride;
         fp.Ic = h->fwl_Ic;
         fp.Iu = h->fwl_Iu;
         fp.err = h->err;
         ieds::fwl_splat_kernel<<<dim3(per_win, nb), ieds::kFwlThreads, 0, st>>>(fp);
         ieds::fwl_reduce_kernel<<<dim3(red_blocks, nb), ieds::kFwlThreads, 0, st>>>(
-            h->fwl_Ic, h->fwl_Iu, npx, h->fwl_acc, h->fwl_accu, comp_image ? comp_image + (size_t)c0 * npx : nullptr);
-        ieds::fwl_finalize_kernel<<<1, 32, 0, st>>>(h->fwl_acc, h->fwl_accu, npx, nb, fwl + c0,
-                                                     var_comp ? var_comp + c0 : nullptr,
-                                                     var_uncomp ? var_uncomp + c0 : nullptr);
+            h->fwl_Ic, h->fwl_Iu, npx, stride, h->fwl_part, red_blocks,
+            comp_image ? comp_image + (size_t)c0 * npx : nullptr);
+        ieds::fwl_finalize_kernel<<<nb, ieds::kFwlThreads, 0, st>>>(h->fwl_part, red_blocks, npx, fwl + c0,
+                                                                     var_comp ? var_comp + c0 : nullptr,
+                                                                     var_uncomp ? var_uncomp + c0 : nullptr);
     }
     e = cudaGetLastError();
     return e == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
