@@ -57,6 +57,17 @@ def _load():
             lib.oracle_window_offsets.restype = i64
             lib.oracle_fwl.argtypes = [P, P, P, i64, i32, i32, P, i64, i64, P, P, P]
             lib.oracle_fwl.restype = i32
+            lib.oracle_downsample.argtypes = [P, i32, i32, P]
+            lib.oracle_upsample_flow.argtypes = [P, i32, i32, i32, i32, P]
+            lib.oracle_warp.argtypes = [P, i32, i32, P, P]
+            lib.oracle_gradients.argtypes = [P, i32, i32, P, P]
+            lib.oracle_hs_jacobi.argtypes = [P, P, P, P, i32, i32, f64, i32, P]
+            lib.oracle_advect_flow.argtypes = [P, i32, i32, P]
+            lib.oracle_flow_levels.argtypes = [i32, i32, i32, P, P]
+            lib.oracle_flow_levels.restype = i64
+            lib.oracle_flow_step.argtypes = [i32, i32, i32, P, P, f64, f64, i32, P, P, P, P]
+            lib.oracle_flow_step.restype = i32
+            lib.oracle_mask_flow.argtypes = [P, P, i64, P, P]
             lib.oracle_alpha_from_dsat.argtypes = [f64]
             lib.oracle_alpha_from_dsat.restype = f64
             lib.oracle_build_window.argtypes = [P, i64, i32, i32, i32, i32, f64, P, P, P, P, P]
@@ -192,6 +203,112 @@ def fwl(xy, t_us, p, width: int, height: int, flow, t_ref_us: int, dt_us: int, i
     if images:
         r["I_comp"], r["I_uncomp"] = ic, iu
     return r
+
+
+# ------------------------------------------------------------------ row f4: flow consumer
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def downsample(I) -> np.ndarray:
+    """2x2 mean pyramid step (reading R21): [H][W] -> [H//2][W//2]."""
+    I = _f64(I)
+    H, W = I.shape
+    out = np.empty((H // 2, W // 2), np.float64)
+    _load().oracle_downsample(_ptr(I), W, H, _ptr(out))
+    return out
+
+
+def upsample_flow(Fc, W: int, H: int) -> np.ndarray:
+    """Half-pixel-centred bilinear upsampling of a [h][w][2] flow to [H][W][2], vectors x2."""
+    Fc = _f64(Fc)
+    h, w = Fc.shape[:2]
+    out = np.empty((H, W, 2), np.float64)
+    _load().oracle_upsample_flow(_ptr(Fc), w, h, W, H, _ptr(out))
+    return out
+
+
+def warp(I, F) -> np.ndarray:
+    """out(p) = bilinear sample of I at p + F(p), coordinates clamped to the frame."""
+    I, F = _f64(I), _f64(F)
+    H, W = I.shape
+    out = np.empty_like(I)
+    _load().oracle_warp(_ptr(I), W, H, _ptr(F), _ptr(out))
+    return out
+
+
+def gradients(J):
+    """Central differences, one-sided on the border: (Ix, Iy)."""
+    J = _f64(J)
+    H, W = J.shape
+    Ix, Iy = np.empty_like(J), np.empty_like(J)
+    _load().oracle_gradients(_ptr(J), W, H, _ptr(Ix), _ptr(Iy))
+    return Ix, Iy
+
+
+def hs_jacobi(Ix, Iy, It, lam: float, K: int, init=None) -> np.ndarray:
+    """K Jacobi sweeps of Horn-Schunck on the total flow from w^0 = init (default 0): [H][W][2]."""
+    Ix, Iy, It = _f64(Ix), _f64(Iy), _f64(It)
+    H, W = Ix.shape
+    ini = _f64(init) if init is not None else None
+    w = np.empty((H, W, 2), np.float64)
+    _load().oracle_hs_jacobi(_ptr(Ix), _ptr(Iy), _ptr(It), _ptr(ini) if ini is not None else None, W, H,
+                             float(lam), int(K), _ptr(w))
+    return w
+
+
+def advect_flow(P) -> np.ndarray:
+    """Pt(p) = P(p - P(p)): a [H][W][2] flow transported by itself (bilinear, border-clamped)."""
+    P = _f64(P)
+    H, W = P.shape[:2]
+    out = np.empty_like(P)
+    _load().oracle_advect_flow(_ptr(P), W, H, _ptr(out))
+    return out
+
+
+def mask_flow(F, E_d):
+    """keep the flow on denoised edge pixels; (masked flow, valid bytes)."""
+    F = _f64(F)
+    E = np.ascontiguousarray(E_d, dtype=np.uint8)
+    out = np.empty_like(F)
+    valid = np.empty(E.shape, np.uint8)
+    _load().oracle_mask_flow(_ptr(F), _ptr(E), E.size, _ptr(out), _ptr(valid))
+    return out, valid
+
+
+class FlowOracle:
+    """Stateful row-f4 estimator (reading R21): feed surfaces window by window with step()."""
+
+    def __init__(self, width: int, height: int, levels=3, lambdas=(500.0, 500.0, 500.0), iters=(20, 20, 20),
+                 gamma: float = 0.5, scale: float = 255.0):
+        self.W, self.H, self.L = width, height, int(levels)
+        self.lam = np.ascontiguousarray(lambdas[:self.L], dtype=np.float64)
+        self.it = np.ascontiguousarray(iters[:self.L], dtype=np.int32)
+        self.gamma, self.scale = float(gamma), float(scale)
+        Ws = np.zeros(16, np.int32)
+        Hs = np.zeros(16, np.int32)
+        tot = _load().oracle_flow_levels(width, height, self.L, _ptr(Ws), _ptr(Hs))
+        if tot < 0:
+            raise ValueError("pyramid level smaller than 2x2")
+        self.sizes = [(int(Ws[l]), int(Hs[l])) for l in range(self.L)]
+        self.prev = np.zeros(tot, np.float64)
+        self.P = np.zeros(2 * tot, np.float64)
+        self.fresh = True
+
+    def reset(self):
+        self.fresh = True
+
+    def step(self, S) -> np.ndarray:
+        S = _f64(S)
+        assert S.shape == (self.H, self.W)
+        F0 = np.empty((self.H, self.W, 2), np.float64)
+        rc = _load().oracle_flow_step(self.W, self.H, self.L, _ptr(self.lam), _ptr(self.it), self.gamma, self.scale,
+                                      1 if self.fresh else 0, _ptr(S), _ptr(self.prev), _ptr(self.P), _ptr(F0))
+        if rc != 0:
+            raise ValueError("oracle_flow_step")
+        self.fresh = False
+        return F0
 
 
 def alpha_from_dsat(d_sat: float) -> float:

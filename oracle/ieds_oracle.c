@@ -424,3 +424,252 @@ int oracle_fwl(const uint32_t *xy, const int64_t *t, const int8_t *p, int64_t n,
     if (!I_uncomp) free(iu);
     return st;
 }
+
+/* ==== Row f4: the flow consumer and the edge masking ===========================
+ * The paper feeds the surfaces to a third-party pyramidal update-prediction optical flow
+ * (Adarve et al.; it "predicts optical flow using an image warping process, and
+ * temporally propagates the optical flow estimations using an incremental framework.
+ * Multiple update-prediction loops are stacked as a pyramidal structure") whose equations the
+ * paper does not give, then restricts the dense flow "to the edge pixels of the denoised edge
+ * image".  The estimator below follows SPEC's declared substitute (pyramid,
+ * warping prediction, incremental regularised brightness-constancy update with per-level
+ * weights and sweeps, temporal propagation with decay gamma), every open choice fixed as
+ * DESIGN reading R21:
+ *   images    J = scale * S (scale = 255: the regularisation weights of P:260 are for 8-bit
+ *             image values), fp64 here;
+ *   pyramid   level l+1 = 2x2 mean of level l, size (W_l / 2, H_l / 2) (floor);
+ *   predict   Pt_l(p) = P_l(p - P_l(p)): the previous window's flow at level l transported by
+ *             itself (bilinear, border-clamped) -- the "image warping" prediction;
+ *   init      coarsest level: Pt_{L-1}; finer levels: upsample(F_{l+1}) -- the bilinear
+ *             sample of F_{l+1} at ((x+0.5)/2 - 0.5, (y+0.5)/2 - 0.5), clamped, times 2;
+ *   warp      J1(p) = J_prev sampled at p - init(p) (SPEC's warp_image, of -init: a
+ *             point at p in the previous window is at p + F in the current one);
+ *   gradients central differences of J1, one-sided on the border; It = J_cur - J1;
+ *   update    K_l Jacobi sweeps of Horn-Schunck on the total flow w (w^0 = init):
+ *             wbar = mean of the 4 neighbours of w (border replicated),
+ *             w <- wbar - (Ix, Iy) (Ix (wbar_u - init_u) + Iy (wbar_v - init_v) + It) / (lambda_l + Ix^2 + Iy^2)
+ *             (w = wbar where the denominator is 0); F_meas,l = w^K;
+ *   filter    F_l = (1 - gamma) F_meas,l + gamma Pt_l  (temporal smoothing);
+ *   state     P_l = F_l for every level; the current pyramid becomes the previous one;
+ *   output    F_0 (pixels per window); the first window of a sequence gives zero flow.
+ *   masking   valid(p) = E_d(p); flow outside the mask is reported as 0. */
+
+static double bl_sample(const double *I, int W, int H, double sx, double sy)
+{
+    if (sx < 0.0) sx = 0.0;
+    if (sx > (double)(W - 1)) sx = (double)(W - 1);
+    if (sy < 0.0) sy = 0.0;
+    if (sy > (double)(H - 1)) sy = (double)(H - 1);
+    int x0 = (int)floor(sx), y0 = (int)floor(sy);
+    double fx = sx - x0, fy = sy - y0;
+    int x1 = x0 + 1 < W ? x0 + 1 : W - 1, y1 = y0 + 1 < H ? y0 + 1 : H - 1;
+    return (1.0 - fx) * (1.0 - fy) * I[(size_t)y0 * W + x0] + fx * (1.0 - fy) * I[(size_t)y0 * W + x1] +
+           (1.0 - fx) * fy * I[(size_t)y1 * W + x0] + fx * fy * I[(size_t)y1 * W + x1];
+}
+
+/* 2x2 mean: out is (W/2) x (H/2) */
+void oracle_downsample(const double *I, int W, int H, double *out)
+{
+    int w = W / 2, h = H / 2;
+    for (int y = 0; y < h; y++)
+        for (int x = 0; x < w; x++)
+            out[(size_t)y * w + x] = (I[(size_t)(2 * y) * W + 2 * x] + I[(size_t)(2 * y) * W + 2 * x + 1] +
+                                      I[(size_t)(2 * y + 1) * W + 2 * x] + I[(size_t)(2 * y + 1) * W + 2 * x + 1]) / 4.0;
+}
+
+/* flow (u, v interleaved) from a w x h level up to W x H, vectors x2 */
+void oracle_upsample_flow(const double *Fc, int w, int h, int W, int H, double *F)
+{
+    double *cu = (double *)malloc(sizeof(double) * (size_t)w * h * 2);
+    double *cv = cu + (size_t)w * h;
+    for (size_t i = 0; i < (size_t)w * h; i++) {
+        cu[i] = Fc[2 * i];
+        cv[i] = Fc[2 * i + 1];
+    }
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            double sx = (x + 0.5) / 2.0 - 0.5, sy = (y + 0.5) / 2.0 - 0.5;
+            F[2 * ((size_t)y * W + x)] = 2.0 * bl_sample(cu, w, h, sx, sy);
+            F[2 * ((size_t)y * W + x) + 1] = 2.0 * bl_sample(cv, w, h, sx, sy);
+        }
+    free(cu);
+}
+
+/* J1(p) = bilinear sample of I at p + F(p), border-clamped */
+void oracle_warp(const double *I, int W, int H, const double *F, double *out)
+{
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            size_t i = (size_t)y * W + x;
+            out[i] = bl_sample(I, W, H, x + F[2 * i], y + F[2 * i + 1]);
+        }
+}
+
+/* central differences, one-sided on the border (0 along an axis of length 1) */
+void oracle_gradients(const double *J, int W, int H, double *Ix, double *Iy)
+{
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            size_t i = (size_t)y * W + x;
+            if (W == 1) Ix[i] = 0.0;
+            else if (x == 0) Ix[i] = J[i + 1] - J[i];
+            else if (x == W - 1) Ix[i] = J[i] - J[i - 1];
+            else Ix[i] = (J[i + 1] - J[i - 1]) / 2.0;
+            if (H == 1) Iy[i] = 0.0;
+            else if (y == 0) Iy[i] = J[i + W] - J[i];
+            else if (y == H - 1) Iy[i] = J[i] - J[i - W];
+            else Iy[i] = (J[i + W] - J[i - W]) / 2.0;
+        }
+}
+
+/* K Jacobi sweeps of Horn-Schunck on the total flow w (u, v interleaved) from w^0 = init:
+ * w <- wbar - grad (grad . (wbar - init) + It) / (lambda + |grad|^2), wbar = 4-neighbour mean
+ * (border replicated); w = wbar where the denominator is 0.  init may be NULL (zero). */
+void oracle_hs_jacobi(const double *Ix, const double *Iy, const double *It, const double *init, int W, int H,
+                      double lambda, int K, double *w)
+{
+    size_t n = (size_t)W * H;
+    double *a = (double *)malloc(sizeof(double) * 2 * n);
+    double *b = (double *)malloc(sizeof(double) * 2 * n);
+    for (size_t i = 0; i < 2 * n; i++) a[i] = init ? init[i] : 0.0;
+    for (int k = 0; k < K; k++) {
+        for (int y = 0; y < H; y++)
+            for (int x = 0; x < W; x++) {
+                size_t i = (size_t)y * W + x;
+                size_t l = x > 0 ? i - 1 : i, r = x < W - 1 ? i + 1 : i;
+                size_t u = y > 0 ? i - W : i, dn = y < H - 1 ? i + W : i;
+                double mu = (a[2 * l] + a[2 * r] + a[2 * u] + a[2 * dn]) / 4.0;
+                double mv = (a[2 * l + 1] + a[2 * r + 1] + a[2 * u + 1] + a[2 * dn + 1]) / 4.0;
+                double den = lambda + Ix[i] * Ix[i] + Iy[i] * Iy[i];
+                if (den > 0.0) {
+                    double iu = init ? init[2 * i] : 0.0, iv = init ? init[2 * i + 1] : 0.0;
+                    double res = Ix[i] * (mu - iu) + Iy[i] * (mv - iv) + It[i];
+                    b[2 * i] = mu - Ix[i] * res / den;
+                    b[2 * i + 1] = mv - Iy[i] * res / den;
+                } else {
+                    b[2 * i] = mu;
+                    b[2 * i + 1] = mv;
+                }
+            }
+        double *t = a;
+        a = b;
+        b = t;
+    }
+    for (size_t i = 0; i < 2 * n; i++) w[i] = a[i];
+    free(a);
+    free(b);
+}
+
+/* Pt(p) = P(p - P(p)) per component (bilinear, border-clamped): the flow transported by itself */
+void oracle_advect_flow(const double *P, int W, int H, double *Pt)
+{
+    size_t n = (size_t)W * H;
+    double *c = (double *)malloc(sizeof(double) * 2 * n);
+    double *cu = c, *cv = c + n;
+    for (size_t i = 0; i < n; i++) {
+        cu[i] = P[2 * i];
+        cv[i] = P[2 * i + 1];
+    }
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            size_t i = (size_t)y * W + x;
+            double sx = x - P[2 * i], sy = y - P[2 * i + 1];
+            Pt[2 * i] = bl_sample(cu, W, H, sx, sy);
+            Pt[2 * i + 1] = bl_sample(cv, W, H, sx, sy);
+        }
+    free(c);
+}
+
+/* level sizes of the pyramid; returns the total pixel count over levels, or -1 if a level
+ * would be smaller than 2 x 2 */
+int64_t oracle_flow_levels(int W, int H, int L, int *Ws, int *Hs)
+{
+    int64_t tot = 0;
+    for (int l = 0; l < L; l++) {
+        Ws[l] = l == 0 ? W : Ws[l - 1] / 2;
+        Hs[l] = l == 0 ? H : Hs[l - 1] / 2;
+        if (Ws[l] < 2 || Hs[l] < 2) return -1;
+        tot += (int64_t)Ws[l] * Hs[l];
+    }
+    return tot;
+}
+
+/* One window of the estimator.  prev_pyr / P are the caller's state (packed levels: level l
+ * at offset sum_{k<l} W_k H_k, flow u,v interleaved); fresh = 1 for the first window.
+ * On return prev_pyr holds the current pyramid and P the per-level flow; F0 = the level-0 flow. */
+int oracle_flow_step(int W, int H, int L, const double *lambda, const int *iters, double gamma, double scale,
+                     int fresh, const double *S, double *prev_pyr, double *P, double *F0)
+{
+    int Ws[16], Hs[16];
+    if (L < 1 || L > 16) return ORACLE_EINVAL;
+    int64_t tot = oracle_flow_levels(W, H, L, Ws, Hs);
+    if (tot < 0) return ORACLE_EINVAL;
+    size_t off[16];
+    off[0] = 0;
+    for (int l = 1; l < L; l++) off[l] = off[l - 1] + (size_t)Ws[l - 1] * Hs[l - 1];
+    double *cur = (double *)malloc(sizeof(double) * (size_t)tot);
+    for (size_t i = 0; i < (size_t)W * H; i++) cur[i] = scale * S[i];
+    for (int l = 1; l < L; l++) oracle_downsample(cur + off[l - 1], Ws[l - 1], Hs[l - 1], cur + off[l]);
+    if (fresh) {
+        for (size_t i = 0; i < (size_t)tot; i++) {
+            prev_pyr[i] = cur[i];
+            P[2 * i] = P[2 * i + 1] = 0.0;
+        }
+        for (size_t i = 0; i < (size_t)W * H * 2; i++) F0[i] = 0.0;
+        free(cur);
+        return ORACLE_OK;
+    }
+    double *Fl = (double *)malloc(sizeof(double) * 2 * (size_t)tot);
+    size_t n0 = (size_t)W * H;
+    double *init = (double *)malloc(sizeof(double) * 2 * n0);
+    double *Pt = (double *)malloc(sizeof(double) * 2 * n0);
+    double *neg = (double *)malloc(sizeof(double) * 2 * n0);
+    double *J1 = (double *)malloc(sizeof(double) * n0);
+    double *Ix = (double *)malloc(sizeof(double) * n0);
+    double *Iy = (double *)malloc(sizeof(double) * n0);
+    double *It = (double *)malloc(sizeof(double) * n0);
+    double *w = (double *)malloc(sizeof(double) * 2 * n0);
+    for (int l = L - 1; l >= 0; l--) {
+        int wl = Ws[l], hl = Hs[l];
+        size_t n = (size_t)wl * hl;
+        oracle_advect_flow(P + 2 * off[l], wl, hl, Pt);
+        if (l == L - 1) {
+            for (size_t i = 0; i < 2 * n; i++) init[i] = Pt[i];
+        } else {
+            oracle_upsample_flow(Fl + 2 * off[l + 1], Ws[l + 1], Hs[l + 1], wl, hl, init);
+        }
+        for (size_t i = 0; i < 2 * n; i++) neg[i] = -init[i];
+        oracle_warp(prev_pyr + off[l], wl, hl, neg, J1);
+        oracle_gradients(J1, wl, hl, Ix, Iy);
+        for (size_t i = 0; i < n; i++) It[i] = cur[off[l] + i] - J1[i];
+        oracle_hs_jacobi(Ix, Iy, It, init, wl, hl, lambda[l], iters[l], w);
+        for (size_t i = 0; i < 2 * n; i++) Fl[2 * off[l] + i] = (1.0 - gamma) * w[i] + gamma * Pt[i];
+    }
+    for (size_t i = 0; i < (size_t)tot; i++) {
+        prev_pyr[i] = cur[i];
+        P[2 * i] = Fl[2 * i];
+        P[2 * i + 1] = Fl[2 * i + 1];
+    }
+    for (size_t i = 0; i < 2 * n0; i++) F0[i] = Fl[i];
+    free(cur);
+    free(Fl);
+    free(init);
+    free(Pt);
+    free(neg);
+    free(J1);
+    free(Ix);
+    free(Iy);
+    free(It);
+    free(w);
+    return ORACLE_OK;
+}
+
+/* P:248 edge masking: valid = E_d (0/1 bytes); flow outside the mask is set to 0 */
+void oracle_mask_flow(const double *F, const uint8_t *E_d, int64_t n, double *out, uint8_t *valid)
+{
+    for (int64_t i = 0; i < n; i++) {
+        valid[i] = E_d[i] ? 1 : 0;
+        out[2 * i] = E_d[i] ? F[2 * i] : 0.0;
+        out[2 * i + 1] = E_d[i] ? F[2 * i + 1] : 0.0;
+    }
+}

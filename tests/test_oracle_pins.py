@@ -474,3 +474,118 @@ def test_fwl_translating_square_spec_example():
     assert r["fwl"] > 1.05
     rnd = np.random.default_rng(4).uniform(-10, 10, (H, W, 2)).astype(np.float32)
     assert oracle.fwl(xy, t, p, W, H, rnd, dt, dt)["fwl"] < 1.0
+
+
+# ---------------------------------------------------------------- row f4: flow consumer
+
+def test_warp_image_spec_examples():
+    """zero flow is the identity; (1,0) on the interior gives I(x+1, y); (0.5,0) on
+    the ramp I = x gives x + 0.5 on the interior; samples beyond the frame clamp to the border."""
+    rng = np.random.default_rng(0)
+    I = rng.random((9, 13))
+    assert np.array_equal(oracle.warp(I, np.zeros((9, 13, 2))), I)
+    F = np.zeros((9, 13, 2)); F[..., 0] = 1.0
+    out = oracle.warp(I, F)
+    assert np.array_equal(out[:, :-1], I[:, 1:]) and np.array_equal(out[:, -1], I[:, -1])
+    ramp = np.tile(np.arange(13, dtype=float), (9, 1))
+    F[..., 0] = 0.5
+    out = oracle.warp(ramp, F)
+    assert np.allclose(out[:, :-1], ramp[:, :-1] + 0.5, atol=0, rtol=0) and np.all(out[:, -1] == 12.0)
+
+
+def test_mask_to_edges_spec_examples():
+    """empty edge image -> nothing valid; all set -> unchanged; half set ->
+    the valid count equals the set count and vectors survive unchanged."""
+    F = np.random.default_rng(1).normal(size=(6, 8, 2))
+    out, v = oracle.mask_flow(F, np.zeros((6, 8), np.uint8))
+    assert v.sum() == 0 and not out.any()
+    out, v = oracle.mask_flow(F, np.ones((6, 8), np.uint8))
+    assert v.all() and np.array_equal(out, F)
+    E = np.zeros((6, 8), np.uint8); E[:, :4] = 1
+    out, v = oracle.mask_flow(F, E)
+    assert v.sum() == 24 and np.array_equal(out[:, :4], F[:, :4]) and not out[:, 4:].any()
+
+
+def test_pyramid_and_gradient_closed_forms():
+    ramp = np.tile(np.arange(8, dtype=float), (6, 1))          # I = x
+    d = oracle.downsample(ramp)                                 # 2x2 mean: (2x + 2x + 1) / 2
+    assert d.shape == (3, 4) and np.array_equal(d, np.tile(2.0 * np.arange(4) + 0.5, (3, 1)))
+    assert oracle.downsample(np.ones((7, 9))).shape == (3, 4)  # floor sizes
+    # upsampling: constant coarse flow c -> 2c; the linear field u_c = x -> 2((x+0.5)/2 - 0.5) = x - 0.5
+    Fc = np.zeros((4, 5, 2)); Fc[..., 0] = 1.5; Fc[..., 1] = -0.25
+    up = oracle.upsample_flow(Fc, 10, 8)
+    assert np.array_equal(up[..., 0], np.full((8, 10), 3.0)) and np.array_equal(up[..., 1], np.full((8, 10), -0.5))
+    Fc[..., 0] = np.arange(5)[None, :]
+    up = oracle.upsample_flow(Fc, 10, 8)
+    assert np.array_equal(up[:, 1:9, 0], np.tile(np.arange(1, 9) - 0.5, (8, 1)))
+    assert np.all(up[:, 0, 0] == 0.0) and np.all(up[:, 9, 0] == 8.0)   # clamped to the coarse border
+    # gradients of 3x + 2y are exactly (3, 2) everywhere (one-sided differences are exact too)
+    yy, xx = np.mgrid[0:5, 0:7].astype(float)
+    Ix, Iy = oracle.gradients(3 * xx + 2 * yy)
+    assert np.all(Ix == 3.0) and np.all(Iy == 2.0)
+    # x^2: central 2x inside, 1 at x = 0, 2W - 3 at x = W - 1
+    Ix, _ = oracle.gradients(xx ** 2)
+    assert np.array_equal(Ix[:, 1:-1], 2 * xx[:, 1:-1]) and np.all(Ix[:, 0] == 1) and np.all(Ix[:, -1] == 11)
+    # transport of a flow by itself: uniform unchanged; u = a x becomes a x (1 - a) inside
+    P = np.zeros((6, 12, 2)); P[..., 0] = 2.0
+    assert np.array_equal(oracle.advect_flow(P), P)
+    P[..., 0] = 0.25 * np.tile(np.arange(12.0), (6, 1))
+    Pt = oracle.advect_flow(P)
+    x = np.arange(12.0)
+    assert np.allclose(Pt[:, 1:, 0], np.tile(0.25 * x[1:] * 0.75, (6, 1)), rtol=0, atol=1e-15)
+
+
+def test_horn_schunck_closed_form():
+    """A ramp a*x translated by d (It = -a (d - c) about a uniform start c): every Jacobi sweep
+    contracts the error by rho = lambda / (lambda + a^2), so w_K = d + (c - d) rho^K exactly."""
+    H, W, a, lam, K = 10, 14, 2.0, 10.0, 15
+    for c, d in ((0.0, 0.7), (0.4, -1.3)):
+        Ix = np.full((H, W), a); Iy = np.zeros((H, W)); It = np.full((H, W), -a * (d - c))
+        init = np.zeros((H, W, 2)); init[..., 0] = c
+        w = oracle.hs_jacobi(Ix, Iy, It, lam, K, init=init)
+        want = d + (c - d) * (lam / (lam + a * a)) ** K
+        assert np.allclose(w[..., 0], want, rtol=0, atol=1e-13) and np.all(w[..., 1] == 0.0)
+
+
+def _square_sequence(W, H, v, n, seed_off=0):
+    from synth.events import pack_xy
+
+    a = oracle.alpha_from_dsat(6.0)
+    out = []
+    for k in range(n):
+        x0 = W // 6 + v * k; y0 = H // 4; s = min(W, H) // 2
+        pts = [(x0 + i, y0) for i in range(s)] + [(x0 + i, y0 + s - 1) for i in range(s)] + \
+              [(x0, y0 + i) for i in range(s)] + [(x0 + s - 1, y0 + i) for i in range(s)]
+        xy = pack_xy(np.array([p[0] for p in pts]), np.array([p[1] for p in pts]))
+        r = oracle.build_window(xy, W, H, 0, 5, a)
+        out.append((r["S"], r["E_d"].astype(bool)))
+    return out
+
+
+def test_flow_estimator_properties():
+    """S:304-306, S:333, S:336 on a square outline's IEDS surfaces (the paper's HD settings:
+    3 levels, weights 500, 20 sweeps; gamma 0.5).  SPEC fixes the motion
+    thresholds from the implementer's run; this one's are written below."""
+    W, H = 256, 192
+    # a static scene: zero flow at every window (fixed point, S:304, S:333)
+    seq = _square_sequence(W, H, 0, 4)
+    fo = oracle.FlowOracle(W, H)
+    for S, _ in seq:
+        assert np.abs(fo.step(S)).max() == 0.0
+    # 1 px/window: after 10 windows the mean over denoised edge pixels is within 0.5 of (1, 0)
+    seq = _square_sequence(W, H, 1, 14)
+    means = {}
+    for g in (0.5, 0.0):
+        fo = oracle.FlowOracle(W, H, gamma=g)
+        ms = [fo.step(S)[E].mean(0) for S, E in seq]
+        means[g] = np.array(ms[6:])
+    assert np.all(np.abs(means[0.5][4:, 0] - 1.0) < 0.5) and np.all(np.abs(means[0.5][:, 1]) < 1e-9)
+    # temporal smoothing (S:336): lower jitter with gamma > 0
+    assert means[0.5][:, 0].std() < means[0.0][:, 0].std()
+    # 8 px/window: the pyramid recovers >= 50 % of the motion, one level < 20 % (this run: 59 % / 10 %)
+    seq = _square_sequence(384, 192, 8, 12)
+    rec = {}
+    for L in (3, 1):
+        fo = oracle.FlowOracle(384, 192, levels=L)
+        rec[L] = np.mean([fo.step(S)[E].mean(0)[0] for S, E in seq][-4:]) / 8.0
+    assert rec[3] >= 0.5 and rec[1] < 0.2
