@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 
-from ._lib import (IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, OUT_FORMATS, TRANSFERS, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
+from ._lib import (IedsFlowConfig, IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, OUT_FORMATS, TRANSFERS, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
                    check, load)
 
 __all__ = ["Builder", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
@@ -237,3 +237,67 @@ class Builder:
                                            off.ctypes.data_as(ctypes.c_void_p), B,
                                            out.ctypes.data_as(ctypes.c_void_p)), "ieds_build_batch_host")
         return out
+
+
+class FlowEstimator:
+    """Row f4 (ieds_flow_*): the stateful flow consumer of the surfaces, DESIGN
+    reading R21.  Defaults are the paper's HD settings (3 levels, weight 500, 20 sweeps
+    each) with gamma = 0.5 and surfaces scaled by 255.  step(surface, edge_bits=None) takes a
+    float32 [H, W] surface (and the uint32 [H, ceil(W/32)] denoised edge bits to restrict the
+    output to) on this device and returns (flow float32 [H, W, 2], valid uint8 [H, W]),
+    enqueued on the current stream; the first window of a sequence gives zero flow."""
+
+    def __init__(self, width: int, height: int, levels: int = 3, lambdas=(500.0, 500.0, 500.0), iterations=(20, 20, 20),
+                 gamma: float = 0.5, scale: float = 255.0, device=None):
+        import torch
+
+        self.width, self.height = int(width), int(height)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        cfg = IedsFlowConfig()
+        cfg.width, cfg.height, cfg.levels = self.width, self.height, int(levels)
+        for l in range(min(int(levels), 8)):
+            cfg.iterations[l] = int(iterations[l])
+            cfg.lambda_[l] = float(lambdas[l])
+        cfg.gamma, cfg.scale, cfg.device = float(gamma), float(scale), self.device.index
+        self._h = ctypes.c_void_p()
+        check(load().ieds_flow_create(ctypes.byref(cfg), ctypes.byref(self._h)), "ieds_flow_create")
+
+    def step(self, surface, edge_bits=None, out=None, stream=None):
+        import torch
+
+        if surface.dtype != torch.float32 or surface.device != self.device or not surface.is_contiguous():
+            raise TypeError("surface must be a contiguous float32 tensor on the estimator's device")
+        if tuple(surface.shape[-2:]) != (self.height, self.width):
+            raise ValueError("surface shape")
+        if edge_bits is not None and (edge_bits.device != self.device or not edge_bits.is_contiguous()):
+            raise TypeError("edge_bits must be a contiguous tensor on the estimator's device")
+        flow = out if out is not None else torch.empty((self.height, self.width, 2), dtype=torch.float32,
+                                                       device=self.device)
+        valid = torch.empty((self.height, self.width), dtype=torch.uint8, device=self.device)
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        check(load().ieds_flow_step(self._h, _ptr(surface), _ptr(edge_bits), _ptr(flow), _ptr(valid),
+                                    ctypes.c_void_p(st)), "ieds_flow_step")
+        return flow, valid
+
+    def reset(self):
+        check(load().ieds_flow_reset(self._h), "ieds_flow_reset")
+
+    def launches_per_step(self) -> int:
+        return int(load().ieds_flow_launches_per_step(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load().ieds_flow_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

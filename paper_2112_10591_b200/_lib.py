@@ -24,8 +24,22 @@ IEDS_NO_EDGE = 0xFFFFFFFF
 # every symbol include/ieds.h declares
 EXPORTS = (
     "ieds_create", "ieds_destroy", "ieds_build_batch", "ieds_build_batch_host", "ieds_sync",
-    "ieds_window_offsets", "ieds_fwl_batch", "ieds_launches_per_batch", "ieds_profile_enable", "ieds_profile_read", "ieds_strerror", "ieds_alpha_from_dsat", "ieds_version",
+    "ieds_window_offsets", "ieds_fwl_batch", "ieds_flow_create", "ieds_flow_destroy", "ieds_flow_reset",
+    "ieds_flow_step", "ieds_flow_launches_per_step", "ieds_launches_per_batch", "ieds_profile_enable", "ieds_profile_read", "ieds_strerror", "ieds_alpha_from_dsat", "ieds_version",
 )
+
+
+class IedsFlowConfig(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int32),
+        ("height", ctypes.c_int32),
+        ("levels", ctypes.c_int32),
+        ("iterations", ctypes.c_int32 * 8),
+        ("lambda_", ctypes.c_double * 8),
+        ("gamma", ctypes.c_double),
+        ("scale", ctypes.c_double),
+        ("device", ctypes.c_int32),
+    ]
 
 
 class IedsConfig(ctypes.Structure):
@@ -89,6 +103,16 @@ def load():
     lib.ieds_window_offsets.restype = ctypes.c_int
     lib.ieds_fwl_batch.argtypes = [P, P, P, P, P, i64, i32, P, P, i64, P, P, P, P, P]
     lib.ieds_fwl_batch.restype = ctypes.c_int
+    lib.ieds_flow_create.argtypes = [P, P]
+    lib.ieds_flow_create.restype = ctypes.c_int
+    lib.ieds_flow_destroy.argtypes = [P]
+    lib.ieds_flow_destroy.restype = None
+    lib.ieds_flow_reset.argtypes = [P]
+    lib.ieds_flow_reset.restype = ctypes.c_int
+    lib.ieds_flow_step.argtypes = [P, P, P, P, P, P]
+    lib.ieds_flow_step.restype = ctypes.c_int
+    lib.ieds_flow_launches_per_step.argtypes = [P]
+    lib.ieds_flow_launches_per_step.restype = i64
     lib.ieds_sync.argtypes = [P, P]
     lib.ieds_sync.restype = ctypes.c_int
     lib.ieds_launches_per_batch.argtypes = [P, i32]

@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ieds.cu")
+SRCS = [SRC, os.path.join(HERE, "csrc", "flow.cu")]   # one shared library, two translation units
 OUT = os.path.join(HERE, "lib", "libieds.so")
 
 NVCC_FLAGS = [
@@ -27,7 +28,7 @@ def nvcc() -> str:
 
 
 def sources():
-    return [SRC] + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "ieds.h")]
+    return SRCS + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "ieds.h")]
 
 
 def up_to_date() -> bool:
@@ -42,7 +43,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
+    cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp] + SRCS
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

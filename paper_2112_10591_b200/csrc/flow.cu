@@ -1,0 +1,344 @@
+// flow.cu -- row f4: the flow consumer of the surfaces and the edge masking
+// of P:248, on the GPU.  The estimator is the substitute of DESIGN reading R21 (
+// the paper's own flow library gives no equations), step for step as oracle_flow_step:
+//
+//   J = scale * S; 2x2-mean pyramid;                   coarse to fine over the levels l:
+//   Pt_l   = P_l(p - P_l(p))                            (previous flow transported by itself)
+//   init   = Pt_{L-1} (coarsest) | 2 * bilinear upsample of F_{l+1}
+//   J1     = J_prev,l sampled at p - init(p)            (border-clamped bilinear)
+//   Ix, Iy = central differences of J1 (one-sided on the border), It = J_cur,l - J1
+//   w      = K_l Jacobi sweeps from init:  w <- wbar - g (g . (wbar - init) + It) / (lambda_l + |g|^2)
+//   F_l    = (1 - gamma) w + gamma Pt_l ;  P_l <- F_l
+//   output = F_0, restricted to the denoised edge pixels E_d when given.
+//
+// fp32 throughout (the oracle is fp64; DESIGN states the tolerance).  One step is ~3 launches
+// from the host: the level-0 scale (reads the caller's surface), one CUDA graph with every
+// per-level kernel (captured once per pyramid parity, replayed each window), and the output /
+// masking pass (writes the caller's buffers).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/ieds.h"
+
+namespace {
+
+constexpr int kFT = 256;   // threads per block for the per-pixel kernels
+constexpr int kMaxLevels = 8;
+
+__device__ __forceinline__ float bl1(const float* __restrict__ I, int W, int H, float sx, float sy) {
+    sx = fminf(fmaxf(sx, 0.f), (float)(W - 1));
+    sy = fminf(fmaxf(sy, 0.f), (float)(H - 1));
+    const int x0 = (int)floorf(sx), y0 = (int)floorf(sy);
+    const float fx = sx - (float)x0, fy = sy - (float)y0;
+    const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+    return (1.f - fx) * (1.f - fy) * I[(size_t)y0 * W + x0] + fx * (1.f - fy) * I[(size_t)y0 * W + x1] +
+           (1.f - fx) * fy * I[(size_t)y1 * W + x0] + fx * fy * I[(size_t)y1 * W + x1];
+}
+
+__device__ __forceinline__ float2 bl2(const float2* __restrict__ I, int W, int H, float sx, float sy) {
+    sx = fminf(fmaxf(sx, 0.f), (float)(W - 1));
+    sy = fminf(fmaxf(sy, 0.f), (float)(H - 1));
+    const int x0 = (int)floorf(sx), y0 = (int)floorf(sy);
+    const float fx = sx - (float)x0, fy = sy - (float)y0;
+    const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+    const float2 a = I[(size_t)y0 * W + x0], b = I[(size_t)y0 * W + x1], c = I[(size_t)y1 * W + x0],
+                 d = I[(size_t)y1 * W + x1];
+    const float wa = (1.f - fx) * (1.f - fy), wb = fx * (1.f - fy), wc = (1.f - fx) * fy, wd = fx * fy;
+    return make_float2(wa * a.x + wb * b.x + wc * c.x + wd * d.x, wa * a.y + wb * b.y + wc * c.y + wd * d.y);
+}
+
+#define IEDS_PIX(W, H)                                                  \
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y; \
+    if (x >= (W) || y >= (H)) return;                                    \
+    const size_t p = (size_t)y * (W) + x;
+
+__global__ void scale_kernel(const float* __restrict__ S, float* __restrict__ J, int W, int H, float s) {
+    IEDS_PIX(W, H)
+    J[p] = s * S[p];
+}
+
+__global__ void down_kernel(const float* __restrict__ src, int Ws, float* __restrict__ dst, int W, int H) {
+    IEDS_PIX(W, H)
+    const float* a = src + (size_t)(2 * y) * Ws + 2 * x;
+    dst[p] = (a[0] + a[1] + a[Ws] + a[Ws + 1]) * 0.25f;
+}
+
+__global__ void advect_kernel(const float2* __restrict__ P, float2* __restrict__ Pt, int W, int H) {
+    IEDS_PIX(W, H)
+    const float2 f = P[p];
+    Pt[p] = bl2(P, W, H, (float)x - f.x, (float)y - f.y);
+}
+
+__global__ void upsample_kernel(const float2* __restrict__ Fc, int Wc, int Hc, float2* __restrict__ F, int W, int H) {
+    IEDS_PIX(W, H)
+    const float2 v = bl2(Fc, Wc, Hc, ((float)x + 0.5f) * 0.5f - 0.5f, ((float)y + 0.5f) * 0.5f - 0.5f);
+    F[p] = make_float2(2.f * v.x, 2.f * v.y);
+}
+
+__global__ void warp_kernel(const float* __restrict__ J, const float2* __restrict__ init, float* __restrict__ J1, int W,
+                            int H) {
+    IEDS_PIX(W, H)
+    const float2 f = init[p];
+    J1[p] = bl1(J, W, H, (float)x - f.x, (float)y - f.y);
+}
+
+// G = (Ix, Iy, It, 1 / (lambda + Ix^2 + Iy^2)) -- 0 where the denominator is 0 (w = wbar there)
+__global__ void grad_kernel(const float* __restrict__ J1, const float* __restrict__ Jc, float4* __restrict__ G, int W,
+                            int H, float lam) {
+    IEDS_PIX(W, H)
+    float ix, iy;
+    if (W == 1) ix = 0.f;
+    else if (x == 0) ix = J1[p + 1] - J1[p];
+    else if (x == W - 1) ix = J1[p] - J1[p - 1];
+    else ix = (J1[p + 1] - J1[p - 1]) * 0.5f;
+    if (H == 1) iy = 0.f;
+    else if (y == 0) iy = J1[p + W] - J1[p];
+    else if (y == H - 1) iy = J1[p] - J1[p - W];
+    else iy = (J1[p + W] - J1[p - W]) * 0.5f;
+    const float den = lam + ix * ix + iy * iy;
+    G[p] = make_float4(ix, iy, Jc[p] - J1[p], den > 0.f ? 1.f / den : 0.f);
+}
+
+__global__ void jacobi_kernel(const float2* __restrict__ win, float2* __restrict__ wout, const float2* __restrict__ init,
+                              const float4* __restrict__ G, int W, int H) {
+    IEDS_PIX(W, H)
+    const float2 l = win[x > 0 ? p - 1 : p], r = win[x < W - 1 ? p + 1 : p];
+    const float2 u = win[y > 0 ? p - W : p], d = win[y < H - 1 ? p + W : p];
+    const float mx = (l.x + r.x + u.x + d.x) * 0.25f, my = (l.y + r.y + u.y + d.y) * 0.25f;
+    const float4 g = G[p];
+    const float2 i0 = init[p];
+    const float res = g.x * (mx - i0.x) + g.y * (my - i0.y) + g.z;
+    wout[p] = make_float2(mx - g.x * res * g.w, my - g.y * res * g.w);
+}
+
+__global__ void blend_kernel(const float2* __restrict__ w, const float2* __restrict__ Pt, float2* __restrict__ F,
+                             int64_t n, float gamma) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float2 a = w[i], b = Pt[i];
+    F[i] = make_float2((1.f - gamma) * a.x + gamma * b.x, (1.f - gamma) * a.y + gamma * b.y);
+}
+
+// caller's outputs: the level-0 flow, restricted to E_d (bit (x % 32) of word [y][x / 32]) when
+// given; `first` = the first window of a sequence (zero flow, nothing valid)
+__global__ void out_kernel(const float2* __restrict__ F0, const uint32_t* __restrict__ Ed, int NW, float2* __restrict__ out,
+                           uint8_t* __restrict__ valid, int W, int H, int first) {
+    IEDS_PIX(W, H)
+    int v = first ? 0 : 1;
+    if (Ed && v) v = (Ed[(size_t)y * NW + (x >> 5)] >> (x & 31)) & 1u;
+    const bool dense = !Ed && !first;
+    out[p] = (v || dense) ? F0[p] : make_float2(0.f, 0.f);
+    if (valid) valid[p] = (uint8_t)v;
+}
+
+inline dim3 pgrid(int W, int H) { return dim3((W + kFT - 1) / kFT, H); }
+
+}  // namespace
+
+struct ieds_flow_handle {
+    ieds_flow_config cfg{};
+    int dev = 0, L = 0;
+    int Ws[kMaxLevels]{}, Hs[kMaxLevels]{};
+    size_t off[kMaxLevels]{}, tot = 0;
+    float* pyr[2] = {nullptr, nullptr};   // ping-pong pyramids (previous / current)
+    float2* P = nullptr;                  // per-level flow (state)
+    float2 *init = nullptr, *Pt = nullptr, *w0 = nullptr, *w1 = nullptr;
+    float* J1 = nullptr;
+    float4* G = nullptr;
+    int cur = 0;                          // pyramid buffer that receives the next window
+    bool fresh = true;
+    cudaStream_t cs = nullptr;            // capture stream
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+struct FlowDevGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit FlowDevGuard(int dev) {
+        ok = cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~FlowDevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// every per-level kernel of one non-first step, reading pyr[1-c] as previous, pyr[c] as current
+void enqueue_levels(ieds_flow_handle* h, int c, cudaStream_t st) {
+    float* cur = h->pyr[c];
+    const float* prev = h->pyr[1 - c];
+    for (int l = 1; l < h->L; ++l)
+        down_kernel<<<pgrid(h->Ws[l], h->Hs[l]), kFT, 0, st>>>(cur + h->off[l - 1], h->Ws[l - 1], cur + h->off[l],
+                                                               h->Ws[l], h->Hs[l]);
+    for (int l = h->L - 1; l >= 0; --l) {
+        const int W = h->Ws[l], H = h->Hs[l];
+        const dim3 g = pgrid(W, H);
+        float2* Pl = h->P + h->off[l];
+        advect_kernel<<<g, kFT, 0, st>>>(Pl, h->Pt, W, H);
+        const float2* init = h->Pt;
+        if (l < h->L - 1) {
+            upsample_kernel<<<g, kFT, 0, st>>>(h->P + h->off[l + 1], h->Ws[l + 1], h->Hs[l + 1], h->init, W, H);
+            init = h->init;
+        }
+        warp_kernel<<<g, kFT, 0, st>>>(prev + h->off[l], init, h->J1, W, H);
+        grad_kernel<<<g, kFT, 0, st>>>(h->J1, cur + h->off[l], h->G, W, H, (float)h->cfg.lambda[l]);
+        // w^0 = init, then K sweeps ping-ponging w0/w1
+        cudaMemcpyAsync(h->w0, init, sizeof(float2) * (size_t)W * H, cudaMemcpyDeviceToDevice, st);
+        float2 *a = h->w0, *b = h->w1;
+        for (int k = 0; k < h->cfg.iterations[l]; ++k) {
+            jacobi_kernel<<<g, kFT, 0, st>>>(a, b, init, h->G, W, H);
+            std::swap(a, b);
+        }
+        const int64_t n = (int64_t)W * H;
+        blend_kernel<<<(unsigned)((n + kFT - 1) / kFT), kFT, 0, st>>>(a, h->Pt, Pl, n, (float)h->cfg.gamma);
+    }
+}
+
+void free_flow(ieds_flow_handle* h) {
+    for (int i = 0; i < 2; ++i) {
+        if (h->gexec[i]) cudaGraphExecDestroy(h->gexec[i]);
+        cudaFree(h->pyr[i]);
+    }
+    cudaFree(h->P);
+    cudaFree(h->init);
+    cudaFree(h->Pt);
+    cudaFree(h->w0);
+    cudaFree(h->w1);
+    cudaFree(h->J1);
+    cudaFree(h->G);
+    if (h->cs) cudaStreamDestroy(h->cs);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ieds_flow_create(const ieds_flow_config* cfg, ieds_flow_handle** out) {
+    if (!out) return IEDS_EINVAL;
+    *out = nullptr;
+    if (!cfg || cfg->levels < 1 || cfg->levels > kMaxLevels || cfg->width < 2 || cfg->height < 2 ||
+        cfg->width > 65535 || cfg->height > 65535)
+        return IEDS_EINVAL;
+    if (!(cfg->gamma >= 0.0 && cfg->gamma <= 1.0) || !(cfg->scale > 0.0) || !std::isfinite(cfg->scale)) return IEDS_EINVAL;
+    auto h = new ieds_flow_handle();
+    h->cfg = *cfg;
+    h->L = cfg->levels;
+    for (int l = 0; l < h->L; ++l) {
+        if (cfg->iterations[l] < 0 || cfg->iterations[l] > 100000 || !(cfg->lambda[l] >= 0.0) ||
+            !std::isfinite(cfg->lambda[l])) {
+            delete h;
+            return IEDS_EINVAL;
+        }
+        h->Ws[l] = l == 0 ? cfg->width : h->Ws[l - 1] / 2;
+        h->Hs[l] = l == 0 ? cfg->height : h->Hs[l - 1] / 2;
+        if (h->Ws[l] < 2 || h->Hs[l] < 2) {
+            delete h;
+            return IEDS_EINVAL;
+        }
+        h->off[l] = h->tot;
+        h->tot += (size_t)h->Ws[l] * h->Hs[l];
+    }
+    int dev = cfg->device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+        delete h;
+        return IEDS_ECUDA;
+    }
+    h->dev = dev;
+    FlowDevGuard g(dev);
+    if (!g.ok) {
+        delete h;
+        return IEDS_ECUDA;
+    }
+    const size_t n0 = (size_t)cfg->width * cfg->height;
+    cudaError_t e = cudaMalloc(&h->pyr[0], sizeof(float) * h->tot);
+    if (e == cudaSuccess) e = cudaMalloc(&h->pyr[1], sizeof(float) * h->tot);
+    if (e == cudaSuccess) e = cudaMalloc(&h->P, sizeof(float2) * h->tot);
+    if (e == cudaSuccess) e = cudaMalloc(&h->init, sizeof(float2) * n0);
+    if (e == cudaSuccess) e = cudaMalloc(&h->Pt, sizeof(float2) * n0);
+    if (e == cudaSuccess) e = cudaMalloc(&h->w0, sizeof(float2) * n0);
+    if (e == cudaSuccess) e = cudaMalloc(&h->w1, sizeof(float2) * n0);
+    if (e == cudaSuccess) e = cudaMalloc(&h->J1, sizeof(float) * n0);
+    if (e == cudaSuccess) e = cudaMalloc(&h->G, sizeof(float4) * n0);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        free_flow(h);
+        delete h;
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? IEDS_ENOMEM : IEDS_ECUDA;
+    }
+    *out = h;
+    return IEDS_OK;
+}
+
+void ieds_flow_destroy(ieds_flow_handle* h) {
+    if (!h) return;
+    FlowDevGuard g(h->dev);
+    cudaDeviceSynchronize();
+    free_flow(h);
+    delete h;
+}
+
+int ieds_flow_reset(ieds_flow_handle* h) {
+    if (!h) return IEDS_EINVAL;
+    h->fresh = true;
+    return IEDS_OK;
+}
+
+int ieds_flow_step(ieds_flow_handle* h, const float* surface, const uint32_t* edge_bits, float* flow, uint8_t* valid,
+                   void* stream) {
+    if (!h || !surface || !flow) return IEDS_EINVAL;
+    FlowDevGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int W = h->cfg.width, H = h->cfg.height, NW = (W + 31) / 32;
+    const int c = h->cur;
+    cudaError_t e = cudaSuccess;
+    scale_kernel<<<pgrid(W, H), kFT, 0, st>>>(surface, h->pyr[c], W, H, (float)h->cfg.scale);
+    const bool first = h->fresh;
+    if (first) {
+        float* cur = h->pyr[c];
+        for (int l = 1; l < h->L; ++l)
+            down_kernel<<<pgrid(h->Ws[l], h->Hs[l]), kFT, 0, st>>>(cur + h->off[l - 1], h->Ws[l - 1], cur + h->off[l],
+                                                                   h->Ws[l], h->Hs[l]);
+        e = cudaMemsetAsync(h->P, 0, sizeof(float2) * h->tot, st);
+    } else {
+        if (!h->gexec[c]) {   // capture this parity's step once
+            cudaGraph_t graph = nullptr;
+            e = cudaStreamBeginCapture(h->cs, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+                enqueue_levels(h, c, h->cs);
+                e = cudaStreamEndCapture(h->cs, &graph);
+            }
+            if (e == cudaSuccess) e = cudaGraphInstantiate(&h->gexec[c], graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return IEDS_ECUDA;
+            }
+        }
+        e = cudaGraphLaunch(h->gexec[c], st);
+    }
+    if (e == cudaSuccess) {
+        out_kernel<<<pgrid(W, H), kFT, 0, st>>>(h->P, edge_bits, NW, reinterpret_cast<float2*>(flow), valid, W, H,
+                                                first ? 1 : 0);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) return IEDS_ECUDA;
+    h->fresh = false;
+    h->cur = 1 - c;
+    return IEDS_OK;
+}
+
+int64_t ieds_flow_launches_per_step(const ieds_flow_handle* h) {
+    if (!h) return 0;
+    int64_t n = 2 + (h->L - 1);   // scale, down kernels, output
+    for (int l = 0; l < h->L; ++l) n += 5 + h->cfg.iterations[l] - (l == h->L - 1 ? 1 : 0);
+    return n;
+}
+
+}  // extern "C"
