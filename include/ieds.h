@@ -106,7 +106,10 @@ typedef struct {
 #define IEDS_FLAG_EXACT_EDT 1
 
 /* Validates cfg, allocates the scratch on cfg->device and builds the Eq. (1) table.
- * On success *out is a new handle; on failure *out is NULL. */
+ * On success *out is a new handle; on failure *out is NULL.
+ * Frame size: one CTA holds a window's whole bit frame in shared memory, so
+ *   4 * (4 + (height + 3) * NWP) + 8 * max(width, NWP) <= 232448 bytes, NWP = (ceil(width/32) + 1) | 1
+ * must hold (1280x720: 129 KB; 1440x1080: 215 KB; 1920x1080 does not fit) -- else IEDS_EINVAL. */
 int ieds_create(const ieds_config *cfg, ieds_handle **out);
 
 /* NULL-safe.  Synchronises the device before freeing. */
