@@ -105,11 +105,19 @@ typedef struct {
  * gives bit-identical surfaces (K_sat = first D2 whose fp32 Eq. (1) value is 1.0f). */
 #define IEDS_FLAG_EXACT_EDT 1
 
+/* Testing aid: split every frame into 64-row bands (one CTA per band, see ieds_create) even
+ * when it fits one CTA, so the banded frame kernel can be checked on small frames. */
+#define IEDS_FLAG_TEST_BANDS 2
+
 /* Validates cfg, allocates the scratch on cfg->device and builds the Eq. (1) table.
  * On success *out is a new handle; on failure *out is NULL.
- * Frame size: one CTA holds a window's whole bit frame in shared memory, so
- *   4 * (4 + (height + 3) * NWP) + 8 * max(width, NWP) <= 232448 bytes, NWP = (ceil(width/32) + 1) | 1
- * must hold (1280x720: 129 KB; 1440x1080: 215 KB; 1920x1080 does not fit) -- else IEDS_EINVAL. */
+ * Frame size: a window's bit frame is held in shared memory by one CTA when
+ *   4 * (4 + (height + 6) * NWP) + 8 * max(width, NWP) <= 232448 bytes, NWP = (ceil(width/32) + 1) | 1
+ * (1280x720: 129 KB); larger frames (1920x1080 and up to 4096x2048) are split into bands of
+ * rows, one CTA each, every band scanning the window's events for its rows plus a 2-row halo.
+ * The exact-EDT kernel (sqdist requests, IEDS_FLAG_EXACT_EDT, the non-saturating transfers)
+ * needs width <= 3968 (16 column segments of <= 255 columns); wider handles serve surfaces
+ * through the streaming kernel and reject sqdist with IEDS_EINVAL. */
 int ieds_create(const ieds_config *cfg, ieds_handle **out);
 
 /* NULL-safe.  Synchronises the device before freeing. */

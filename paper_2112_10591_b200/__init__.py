@@ -55,7 +55,7 @@ class Builder:
 
     def __init__(self, width: int, height: int, n_d: int, n_f: int, alpha: float | None = None,
                  d_sat: float = 6.0, chunk_windows: int = 0, device=None, exact_edt: bool = False,
-                 transfer: str = "invexp", bound: float = 6.0, out: str = "f32"):
+                 transfer: str = "invexp", bound: float = 6.0, out: str = "f32", _test_bands: bool = False):
         import torch
 
         if not torch.cuda.is_available():
@@ -69,7 +69,8 @@ class Builder:
         if transfer not in TRANSFERS or out not in OUT_FORMATS:
             raise ValueError(f"transfer must be one of {list(TRANSFERS)}, out one of {list(OUT_FORMATS)}")
         cfg = IedsConfig(width, height, n_d, n_f, float(alpha), chunk_windows, self.device.index,
-                         IEDS_FLAG_EXACT_EDT if exact_edt else 0, TRANSFERS[transfer], float(bound),
+                         (IEDS_FLAG_EXACT_EDT if exact_edt else 0) | (2 if _test_bands else 0),
+                         TRANSFERS[transfer], float(bound),
                          OUT_FORMATS[out])
         self.out = out
         self.transfer = transfer

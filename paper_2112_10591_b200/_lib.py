@@ -59,6 +59,7 @@ class IedsConfig(ctypes.Structure):
 
 
 IEDS_FLAG_EXACT_EDT = 1
+IEDS_FLAG_TEST_BANDS = 2   # testing aid: 64-row frame bands even when the frame fits one CTA
 TRANSFERS = {"invexp": 0, "linear": 1, "bounded": 2, "log": 3}   # IEDS_TRANSFER_*
 OUT_FORMATS = {"f32": 0, "u8": 1, "f16": 2}                         # IEDS_OUT_*
 

@@ -6,12 +6,17 @@
 //   then         E_df is transposed into column words T (bit i of T[r][x] = E_df(x, 32r+i))
 //                plus a per-column bitmap of non-empty word-rows, which is all the EDT needs.
 //
-// Layout: the frame lives in shared memory as H + 3 rows of NWP words, NWP = the smallest odd
-// number > ceil(W/32) (an odd row stride makes the "lane = row" accesses bank-conflict free and
-// leaves at least one zero pad word per row), after 4 zero words (so word -1 of row -1 reads 0).
-// Frame row y is shared row y + 1; rows 0, H+1, H+2 and the pad words are zero, so
-// out-of-frame neighbours read as non-edge (reading R1) without bounds checks.  Bit (x % 32) of
-// word x / 32 is pixel x; bits beyond W stay 0.
+// Layout: one CTA per (window, row band).  Band k covers frame rows [ylo, yhi) =
+// [k * BR, min(H, (k + 1) * BR)) (BR = band_rows, a multiple of 32 when there are several bands;
+// one band = the whole frame for every frame that fits, 1280x720 included).  Its shared-memory
+// frame holds rows ylo - 3 .. yhi + 2 (a zero guard row, the two-row halo Alg. 1 + Alg. 2
+// need on each side, and a zero guard row), BR + 6 rows of NWP words, after 4 zero words (so
+// word -1 of the first row reads 0).  NWP = the smallest odd number > ceil(W/32): an odd row
+// stride makes the "lane = row" accesses bank-conflict free and leaves at least one zero pad
+// word per row.  fr1 points where frame row 0 would be, so frame row y is fr1 + y * NWP for
+// every row the band touches; rows outside the frame and the pad words are zero, so
+// out-of-frame neighbours read as non-edge (reading R1) without bounds checks.  Bit (x % 32)
+// of word x / 32 is pixel x; bits beyond W stay 0.
 #pragma once
 #include <cstdint>
 
@@ -26,6 +31,7 @@ struct FrameParams {
     const int64_t* __restrict__ offsets;    // [nb + 1] absolute indices into xy
     int64_t n_events;
     int W, H, NW, NWP, NR, n_d, n_f;
+    int band_rows, nbands;                  // rows per band (see Layout), bands per window
     int vec_ok;                             // xy is 16-byte aligned
     uint32_t* __restrict__ T;               // [nb][NR][W] transposed E_df
     unsigned long long* __restrict__ colmask;  // [nb][W] bit r = T[r][x] != 0
@@ -49,8 +55,9 @@ __device__ __forceinline__ uint32_t at_least(int n, uint32_t a, uint32_t b, uint
     }
 }
 
-__device__ __forceinline__ uint32_t frame_word(const uint32_t* fr, const FrameParams& p, int y, int w) {
-    return (y >= 0 && y < p.H && w >= 0 && w < p.NW) ? fr[(y + 1) * p.NWP + w] : 0u;
+// frame word (y, w) through fr1 (frame row 0; see Layout), 0 outside the frame
+__device__ __forceinline__ uint32_t frame_word(const uint32_t* fr1, const FrameParams& p, int y, int w) {
+    return (y >= 0 && y < p.H && w >= 0 && w < p.NW) ? fr1[y * p.NWP + w] : 0u;
 }
 
 // E_d word (y, w): Alg. 1 on 32 pixels at once.
@@ -63,13 +70,20 @@ __device__ __forceinline__ uint32_t denoised_word(const uint32_t* fr, const Fram
     return c & at_least(p.n_d, up, dn, lf, rt);
 }
 
-// Sets the event's pixel; returns nonzero if the event is outside the frame.  Branch-free: the
-// coordinates are clamped into the frame with one packed min (lim = (H-1) << 16 | (W-1)) and an
-// out-of-frame event ORs nothing.
-__device__ __forceinline__ uint32_t scatter_event(uint32_t* fr1, uint32_t lim, int NWP, uint32_t v) {
+// Sets the event's pixel if its row is one of the band's (ylo - 2 <= y < yhi + 2); returns
+// nonzero if the event is outside the frame.  Branch-free: the coordinates are clamped into the
+// frame with one packed min (lim = (H-1) << 16 | (W-1)), the row into the band, and an event
+// outside either ORs nothing.
+template <bool BANDED>
+__device__ __forceinline__ uint32_t scatter_event(uint32_t* fr1, uint32_t lim, int NWP, int ya, int yb, uint32_t v) {
     const uint32_t c = __vminu2(v, lim);
-    const uint32_t x = c & 0xFFFFu, y = c >> 16;
-    atomicOr(&fr1[y * NWP + (x >> 5)], c == v ? 1u << (x & 31) : 0u);
+    const int x = (int)(c & 0xFFFFu), y = (int)(c >> 16);
+    if constexpr (BANDED) {
+        const int yc = min(max(y, ya), yb);
+        atomicOr(&fr1[yc * NWP + (x >> 5)], (c == v && yc == y) ? 1u << (x & 31) : 0u);
+    } else {   // one band holds every row
+        atomicOr(&fr1[y * NWP + (x >> 5)], c == v ? 1u << (x & 31) : 0u);
+    }
     return c ^ v;
 }
 
@@ -170,14 +184,14 @@ __device__ __forceinline__ void df_walk(const uint32_t* fr1, const FrameParams& 
 
 // the default path's a2 + a3: word columns x row bands over the CTA's threads
 template <int ND, int NF>
-__device__ __forceinline__ void denoise_fill_walk(const uint32_t* fr1, const FrameParams& p, int b, int tid,
-                                                  int nthr) {
-    const int NW = p.NW, H = p.H;
+__device__ __forceinline__ void denoise_fill_walk(const uint32_t* fr1, const FrameParams& p, int b, int ylo, int yhi,
+                                                  int tid, int nthr) {
+    const int NW = p.NW;
     const int nbands = nthr / NW;   // >= 1 (host: NW <= threads)
     const int band = tid / NW, w = tid - band * NW;
     if (band >= nbands) return;
-    const int rows = (H + nbands - 1) / nbands;
-    const int y0 = band * rows, y1 = min(H, y0 + rows);
+    const int rows = (yhi - ylo + nbands - 1) / nbands;
+    const int y0 = ylo + band * rows, y1 = min(yhi, y0 + rows);
     if (y0 >= y1) return;
     const uint32_t wmask = (w == NW - 1 && (p.W & 31)) ? ((1u << (p.W & 31)) - 1u) : kFull;
     if (p.Ed_out || p.Edf_out)
@@ -187,33 +201,70 @@ __device__ __forceinline__ void denoise_fill_walk(const uint32_t* fr1, const Fra
 }
 
 template <int ND>
-__device__ __forceinline__ void denoise_fill_nf(const uint32_t* fr1, const FrameParams& p, int b, int tid, int nthr) {
+__device__ __forceinline__ void denoise_fill_nf(const uint32_t* fr1, const FrameParams& p, int b, int ylo, int yhi,
+                                                int tid, int nthr) {
     switch (p.n_f) {
-        case 1: denoise_fill_walk<ND, 1>(fr1, p, b, tid, nthr); break;
-        case 2: denoise_fill_walk<ND, 2>(fr1, p, b, tid, nthr); break;
-        case 3: denoise_fill_walk<ND, 3>(fr1, p, b, tid, nthr); break;
-        case 4: denoise_fill_walk<ND, 4>(fr1, p, b, tid, nthr); break;
-        default: denoise_fill_walk<ND, 5>(fr1, p, b, tid, nthr); break;
+        case 1: denoise_fill_walk<ND, 1>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        case 2: denoise_fill_walk<ND, 2>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        case 3: denoise_fill_walk<ND, 3>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        case 4: denoise_fill_walk<ND, 4>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        default: denoise_fill_walk<ND, 5>(fr1, p, b, ylo, yhi, tid, nthr); break;
     }
 }
 
-__device__ __forceinline__ void streaming_denoise_fill(const uint32_t* fr1, const FrameParams& p, int b, int tid,
-                                                       int nthr) {
+__device__ __forceinline__ void streaming_denoise_fill(const uint32_t* fr1, const FrameParams& p, int b, int ylo,
+                                                       int yhi, int tid, int nthr) {
     switch (p.n_d) {
-        case 0: denoise_fill_nf<0>(fr1, p, b, tid, nthr); break;
-        case 1: denoise_fill_nf<1>(fr1, p, b, tid, nthr); break;
-        case 2: denoise_fill_nf<2>(fr1, p, b, tid, nthr); break;
-        case 3: denoise_fill_nf<3>(fr1, p, b, tid, nthr); break;
-        default: denoise_fill_nf<4>(fr1, p, b, tid, nthr); break;
+        case 0: denoise_fill_nf<0>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        case 1: denoise_fill_nf<1>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        case 2: denoise_fill_nf<2>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        case 3: denoise_fill_nf<3>(fr1, p, b, ylo, yhi, tid, nthr); break;
+        default: denoise_fill_nf<4>(fr1, p, b, ylo, yhi, tid, nthr); break;
     }
+}
+
+// a1 for one window (and band): every event of [o0, o1), 16-byte streaming loads with 4 in
+// flight per thread; returns nonzero if any event lies outside the frame
+template <bool BANDED>
+__device__ __forceinline__ uint32_t scatter_window(uint32_t* fr1, const FrameParams& p, int64_t o0, int64_t o1, int ya,
+                                                   int yb, int tid, int nthr) {
+    uint32_t bad = 0;
+    const uint32_t lim = ((uint32_t)(p.H - 1) << 16) | (uint32_t)(p.W - 1);
+    const int NWP = p.NWP;
+    if (p.vec_ok) {
+        int64_t h1 = o1 < ((o0 + 3) & ~3ll) ? o1 : ((o0 + 3) & ~3ll);
+        int64_t v1 = h1 > (o1 & ~3ll) ? h1 : (o1 & ~3ll);
+        for (int64_t i = o0 + tid; i < h1; i += nthr) bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, __ldg(p.xy + i));
+        const uint4* x4 = reinterpret_cast<const uint4*>(p.xy);
+        int64_t j = (h1 >> 2) + tid;
+        const int64_t j1 = v1 >> 2;
+        for (; j + 3 * nthr < j1; j += 4 * nthr) {   // 4 loads in flight per thread
+            uint4 q0 = ld_stream_u4(x4 + j), q1 = ld_stream_u4(x4 + j + nthr);
+            uint4 q2 = ld_stream_u4(x4 + j + 2 * nthr), q3 = ld_stream_u4(x4 + j + 3 * nthr);
+            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.w);
+            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.w);
+            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.w);
+            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.w);
+        }
+        for (; j < j1; j += nthr) {
+            uint4 q = ld_stream_u4(x4 + j);
+            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.w);
+        }
+        for (int64_t i = v1 + tid; i < o1; i += nthr) bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, __ldg(p.xy + i));
+    } else {
+        for (int64_t i = o0 + tid; i < o1; i += nthr) bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, __ldg(p.xy + i));
+    }
+    return bad;
 }
 
 __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    const int nframe = 4 + (p.H + 3) * p.NWP;   // 4 zero words, then the frame (see Layout)
+    const int nframe = 4 + (p.band_rows + 6) * p.NWP;   // 4 zero words, then the band's rows (see Layout)
     uint32_t* fr = smem + 4;
     unsigned long long* cm = reinterpret_cast<unsigned long long*>(smem + ((nframe + 3) & ~3));
     const int b = blockIdx.x;
+    const int ylo = blockIdx.y * p.band_rows, yhi = min(p.H, ylo + p.band_rows);
+    const int ya = max(0, ylo - 2), yb = min(p.H - 1, yhi + 1);   // frame rows this band stores
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
 
@@ -223,7 +274,8 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
         uint4* f4 = reinterpret_cast<uint4*>(fr);
         const int n4 = (nframe + 3) >> 2;
         for (int i = tid; i < n4; i += nthr) f4[i] = z;
-        for (int i = tid; i < p.W; i += nthr) cm[i] = 0ull;
+        if (p.T)
+            for (int i = tid; i < p.W; i += nthr) cm[i] = 0ull;
     }
     __syncthreads();
 
@@ -233,56 +285,36 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
         if (tid == 0) atomicOr(p.err, kErrOrder);
         o0 = o1 = 0;
     }
-    uint32_t bad = 0;
-    uint32_t* fr1 = fr + p.NWP;   // frame row 0
-    const uint32_t lim = ((uint32_t)(p.H - 1) << 16) | (uint32_t)(p.W - 1);
-    const int NWP = p.NWP;
-    if (p.vec_ok) {
-        int64_t h1 = o1 < ((o0 + 3) & ~3ll) ? o1 : ((o0 + 3) & ~3ll);
-        int64_t v1 = h1 > (o1 & ~3ll) ? h1 : (o1 & ~3ll);
-        for (int64_t i = o0 + tid; i < h1; i += nthr) bad |= scatter_event(fr1, lim, NWP, __ldg(p.xy + i));
-        const uint4* x4 = reinterpret_cast<const uint4*>(p.xy);
-        int64_t j = (h1 >> 2) + tid;
-        const int64_t j1 = v1 >> 2;
-        for (; j + 3 * nthr < j1; j += 4 * nthr) {   // 4 loads in flight per thread
-            uint4 q0 = ld_stream_u4(x4 + j), q1 = ld_stream_u4(x4 + j + nthr);
-            uint4 q2 = ld_stream_u4(x4 + j + 2 * nthr), q3 = ld_stream_u4(x4 + j + 3 * nthr);
-            bad |= scatter_event(fr1, lim, NWP, q0.x) | scatter_event(fr1, lim, NWP, q0.y) | scatter_event(fr1, lim, NWP, q0.z) | scatter_event(fr1, lim, NWP, q0.w);
-            bad |= scatter_event(fr1, lim, NWP, q1.x) | scatter_event(fr1, lim, NWP, q1.y) | scatter_event(fr1, lim, NWP, q1.z) | scatter_event(fr1, lim, NWP, q1.w);
-            bad |= scatter_event(fr1, lim, NWP, q2.x) | scatter_event(fr1, lim, NWP, q2.y) | scatter_event(fr1, lim, NWP, q2.z) | scatter_event(fr1, lim, NWP, q2.w);
-            bad |= scatter_event(fr1, lim, NWP, q3.x) | scatter_event(fr1, lim, NWP, q3.y) | scatter_event(fr1, lim, NWP, q3.z) | scatter_event(fr1, lim, NWP, q3.w);
-        }
-        for (; j < j1; j += nthr) {
-            uint4 q = ld_stream_u4(x4 + j);
-            bad |= scatter_event(fr1, lim, NWP, q.x) | scatter_event(fr1, lim, NWP, q.y) | scatter_event(fr1, lim, NWP, q.z) | scatter_event(fr1, lim, NWP, q.w);
-        }
-        for (int64_t i = v1 + tid; i < o1; i += nthr) bad |= scatter_event(fr1, lim, NWP, __ldg(p.xy + i));
-    } else {
-        for (int64_t i = o0 + tid; i < o1; i += nthr) bad |= scatter_event(fr1, lim, NWP, __ldg(p.xy + i));
-    }
+    uint32_t* fr1 = fr + (3 - ylo) * p.NWP;   // where frame row 0 would be (shared row 3 - ylo)
+    const uint32_t bad = p.nbands == 1 ? scatter_window<false>(fr1, p, o0, o1, ya, yb, tid, nthr)
+                                       : scatter_window<true>(fr1, p, o0, o1, ya, yb, tid, nthr);
     if (bad) atomicOr(p.err, kErrRange);
     __syncthreads();
 
     if (p.E_out) {
         uint32_t* out = p.E_out + (size_t)b * p.H * p.NW;
-        for (int i = tid; i < p.H * p.NW; i += nthr) out[i] = fr[(i / p.NW + 1) * p.NWP + (i % p.NW)];
+        const int n = (yhi - ylo) * p.NW;
+        for (int i = tid; i < n; i += nthr) {
+            const int y = ylo + i / p.NW, w = i % p.NW;
+            out[(size_t)y * p.NW + w] = fr1[y * p.NWP + w];
+        }
     }
 
     if (!p.T) {   // streaming surface path: row-major E_df only
-        streaming_denoise_fill(fr1, p, b, tid, nthr);
+        streaming_denoise_fill(fr1, p, b, ylo, yhi, tid, nthr);
         return;
     }
 
     // ---- a2 + a3 on 32x32 blocks (lane = row), then transpose the block into T
     const uint32_t lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : kFull;
-    const int nitems = p.NR * p.NW;
+    const int r0 = ylo / 32, nitems = ((yhi + 31) / 32 - r0) * p.NW;   // this band's word rows
     for (int item = warp; item < nitems; item += nwarps) {
-        const int r = item / p.NW, w = item - r * p.NW;
+        const int r = r0 + item / p.NW, w = item % p.NW;
         const int y = 32 * r + lane;
-        const uint32_t cd = denoised_word(fr, p, y, w);
-        const uint32_t ld = denoised_word(fr, p, y, w - 1);
-        const uint32_t rd = denoised_word(fr, p, y, w + 1);
-        const uint32_t xd = denoised_word(fr, p, lane == 0 ? 32 * r - 1 : 32 * r + 32, w);
+        const uint32_t cd = denoised_word(fr1, p, y, w);
+        const uint32_t ld = denoised_word(fr1, p, y, w - 1);
+        const uint32_t rd = denoised_word(fr1, p, y, w + 1);
+        const uint32_t xd = denoised_word(fr1, p, lane == 0 ? 32 * r - 1 : 32 * r + 32, w);
         uint32_t up = __shfl_up_sync(kFull, cd, 1);
         uint32_t dn = __shfl_down_sync(kFull, cd, 1);
         if (lane == 0) up = xd;
@@ -304,7 +336,10 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
         }
     }
     __syncthreads();
-    for (int x = tid; x < p.W; x += nthr) p.colmask[(size_t)b * p.W + x] = cm[x];
+    for (int x = tid; x < p.W; x += nthr) {
+        if (p.nbands == 1) p.colmask[(size_t)b * p.W + x] = cm[x];
+        else if (cm[x]) atomicOr(&p.colmask[(size_t)b * p.W + x], cm[x]);   // zeroed by the host
+    }
 }
 
 }  // namespace ieds

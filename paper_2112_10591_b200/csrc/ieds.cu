@@ -58,6 +58,7 @@ struct ieds_handle {
     ieds_config cfg;
     int dev;
     int NW, NWP, NR, NS, SEGW;
+    int band_rows, nbands;     // frame kernel: rows per CTA band, bands per window (frame_kernel.cuh)
     int chunk;        // windows per launch pair of the device path (scratch capacity)
     int host_chunk;   // windows per pipelined copy/compute step of the host path (<= chunk)
     size_t smem_frame, smem_edt, smem_edt_d2;
@@ -65,6 +66,7 @@ struct ieds_handle {
     int c_win;                 // window size of the branch-free kernel (>= c_sat)
     bool streaming;            // saturation-aware window kernel usable (K_sat <= 1024)
     bool norm_u8;              // 8-bit view of Id / min / ln normalised by the frame maximum
+    bool exact_ok;             // the exact-EDT kernel fits this width (sqdist requests need it)
     uint32_t* D2n = nullptr;   // norm_u8: [chunk][H][W] exact D2 scratch
     uint32_t* wmax = nullptr;  // norm_u8: [chunk] per-window max D2
     double* vtab = nullptr;    // norm_u8: [(W-1)^2 + (H-1)^2 + 1] fp64 transfer of every D2
@@ -259,6 +261,8 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     fp.NW = h->NW;
     fp.NWP = h->NWP;
     fp.NR = h->NR;
+    fp.band_rows = h->band_rows;
+    fp.nbands = h->nbands;
     fp.n_d = h->cfg.n_d;
     fp.n_f = h->cfg.n_f;
     fp.vec_ok = ((reinterpret_cast<uintptr_t>(xy) & 15u) == 0) ? 1 : 0;
@@ -278,7 +282,9 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     cudaEvent_t pa, pb;
     prof_pair(h, 0, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
-    ieds::frame_kernel<<<nb, kFrameThreads, h->smem_frame, st>>>(fp);
+    if (!stream_path && h->nbands > 1)   // bands OR their word rows into the column bitmap
+        cudaMemsetAsync(h->colmask, 0, sizeof(unsigned long long) * (size_t)nb * h->cfg.width, st);
+    ieds::frame_kernel<<<dim3(nb, h->nbands), kFrameThreads, h->smem_frame, st>>>(fp);
     if (pb) cudaEventRecord(pb, st);
 
     if (stream_path) {
@@ -370,7 +376,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (W < 1 || W > 4096 || H < 1 || H > 2048) return IEDS_EINVAL;
     if (cfg->n_d < 0 || cfg->n_d > 4 || cfg->n_f < 1 || cfg->n_f > 5) return IEDS_EINVAL;
     if (!(cfg->alpha > 0.0) || !std::isfinite(cfg->alpha)) return IEDS_EINVAL;
-    if (cfg->chunk_windows < 0 || (cfg->flags & ~IEDS_FLAG_EXACT_EDT)) return IEDS_EINVAL;
+    if (cfg->chunk_windows < 0 || (cfg->flags & ~(IEDS_FLAG_EXACT_EDT | IEDS_FLAG_TEST_BANDS))) return IEDS_EINVAL;
     if (cfg->transfer < IEDS_TRANSFER_INVEXP || cfg->transfer > IEDS_TRANSFER_LOG) return IEDS_EINVAL;
     if (cfg->transfer == IEDS_TRANSFER_BOUNDED && !(cfg->bound > 0.0 && std::isfinite(cfg->bound)))
         return IEDS_EINVAL;
@@ -419,12 +425,29 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) && !h->norm_u8 &&
                    ieds::window_smem_bytes(H) <= (size_t)kMaxSmem;
 
-    // 4 zero words + frame (H + 3 rows), then the column bitmap of the exact path
-    h->smem_frame = 4ull * ((4 + (H + 3) * h->NWP + 3) & ~3) + 8ull * std::max(W, h->NWP);
+    // 4 zero words + the band's frame rows (band_rows + 6), then the column bitmap of the exact
+    // path.  One band holds the whole frame whenever that fits (1280x720: 129 KB); larger
+    // frames are split into the fewest bands of a multiple of 32 rows that fit.
+    auto frame_bytes = [&](int br) {
+        return 4ull * ((4 + (size_t)(br + 6) * h->NWP + 3) & ~3ull) + 8ull * std::max(W, h->NWP);
+    };
+    h->band_rows = H;
+    h->nbands = 1;
+    if (frame_bytes(H) > (size_t)kMaxSmem || (cfg->flags & IEDS_FLAG_TEST_BANDS)) {
+        int br = (cfg->flags & IEDS_FLAG_TEST_BANDS) ? 64 : ((H + 31) / 32) * 32;
+        while (br > 32 && frame_bytes(br) > (size_t)kMaxSmem) br -= 32;
+        const int nb = (H + br - 1) / br;
+        h->band_rows = ((H + nb - 1) / nb + 31) / 32 * 32;   // balanced, still a multiple of 32
+        h->nbands = (H + h->band_rows - 1) / h->band_rows;
+    }
+    h->smem_frame = frame_bytes(h->band_rows);
     h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
     h->smem_edt_d2 = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, true);
-    if (h->smem_frame > (size_t)kMaxSmem || h->smem_edt_d2 > (size_t)kMaxSmem || h->SEGW > 255 ||
-        h->NW > kFrameThreads) {   // the D&F walk gives every word column a thread
+    // the exact EDT keeps 1-byte site offsets per segment (<= 255 columns) and its per-row data
+    // in shared memory; without it the handle still serves the streaming path (no sqdist)
+    h->exact_ok = h->smem_edt_d2 <= (size_t)kMaxSmem && h->SEGW <= 255;
+    if (h->smem_frame > (size_t)kMaxSmem || h->NW > kFrameThreads ||   // the D&F walk: a thread per word column
+        (!h->exact_ok && (!h->streaming || (cfg->flags & IEDS_FLAG_EXACT_EDT)))) {
         delete h;
         return IEDS_EINVAL;
     }
@@ -544,6 +567,7 @@ int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* w
     if ((reinterpret_cast<uintptr_t>(events_xy) & 3u) ||
         (reinterpret_cast<uintptr_t>(surfaces) & (out_elem_bytes(h) - 1)))
         return IEDS_EINVAL;
+    if (sqdist && !h->exact_ok) return IEDS_EINVAL;
     DeviceGuard g(h->dev);
     if (!g.ok) return IEDS_ECUDA;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

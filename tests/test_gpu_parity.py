@@ -32,7 +32,7 @@ def unpack(bits, W, H):
     return full[:, :W]
 
 
-def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True, exact_edt=False):
+def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True, exact_edt=False, bands=False):
     """Run the CUDA path.  With debug=True the intermediate frames and D2 are requested (this
     selects the exact-EDT kernel) and the surface-only call (default streaming kernel) is run
     as well: the two surfaces must be bit-identical."""
@@ -52,7 +52,8 @@ def run_gpu(xy, off, W, H, n_d, n_f, alpha, chunk=0, xy_shift=0, debug=True, exa
         outs["D2"] = torch.full((B, H, W), 7, dtype=torch.int32, device=dev)
     S = torch.full((B, H, W), -5.0, dtype=torch.float32, device=dev)
     S2 = torch.full((B, H, W), -5.0, dtype=torch.float32, device=dev)
-    with ieds().Builder(W, H, n_d, n_f, alpha=alpha, chunk_windows=chunk, device=0, exact_edt=exact_edt) as bld:
+    with ieds().Builder(W, H, n_d, n_f, alpha=alpha, chunk_windows=chunk, device=0, exact_edt=exact_edt,
+                        _test_bands=bands) as bld:
         bld.build_batch(txy, toff, S2)
         if debug:
             bld.build_batch(txy, toff, S, edge_bits=outs.get("E"), denoised_bits=outs.get("E_d"),
@@ -301,3 +302,45 @@ def test_streaming_surface_bit_identical_to_exact(d_sat):
     for b in (0, 6, 9):
         ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, 0, 5, a)
         assert np.abs(g_stream["S"][b] - ref["S"]).max() <= TOL
+
+
+# ----------------------------------------------------------------------------- banded frames
+
+@pytest.mark.parametrize("name,nwin", [("C1", 4), ("C3", 2), ("C5", 1)])
+def test_banded_frame_kernel_forced(name, nwin):
+    """IEDS_FLAG_TEST_BANDS splits the frame into 64-row bands (one CTA each, halo of 2 rows):
+    E / E_d / E_df / D2 bit-exact and the surface within 2e-6 on both the exact and the
+    streaming path, exactly as with one band."""
+    wl = WORKLOADS[name]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 11, nwin)
+    gpu = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, a, bands=True)
+    one = run_gpu(xy, off, c.width, c.height, wl.n_d, wl.n_f, a, bands=False)
+    for b in range(nwin):
+        check_window(gpu, b, xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a)
+    for k in ("S", "E", "E_d", "E_df", "D2"):
+        assert np.array_equal(gpu[k], one[k]), k
+
+
+def test_full_hd_1920x1080_uses_bands():
+    """1920x1080 does not fit one CTA's shared memory: the frame kernel splits it into row
+    bands.  Parity against the oracle on two windows of a Gen4-like scene at that size."""
+    c = SceneConfig(1920, 1080, 150_000, n_prims=140, len_range=(30.0, 300.0), sigma=0.55,
+                    noise_frac=0.10, vmax=8.0, dt_us=15000)
+    a = oracle.alpha_from_dsat(6.0)
+    xy, off = batch_events(c, 21, 0, 2)
+    gpu = run_gpu(xy, off, c.width, c.height, 2, 3, a)
+    for b in range(2):
+        check_window(gpu, b, xy[off[b]:off[b + 1]], c.width, c.height, 2, 3, a)
+
+
+def test_largest_frames_create():
+    """The header's largest geometry (4096 x 2048) builds a handle and an empty window."""
+    torch = _torch()
+    with ieds().Builder(4096, 2048, 1, 4, device=0) as bld:
+        S = bld.build_batch(torch.zeros(4, dtype=torch.int32, device="cuda"),
+                            torch.zeros(2, dtype=torch.int64, device="cuda"))
+        bld.sync()
+        assert bool((S == 1.0).all())
+
