@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -31,8 +32,12 @@ namespace {
 constexpr int kFrameThreads = 1024;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
 constexpr int kLutMax = ieds::kWinLutMax;
-constexpr int kSegTarget = 80;
-constexpr int kFwlChunk = 8;       // row f3: windows per splat/reduce pass (12 B/px of L2 scratch each)     // columns per EDT segment (warp)
+constexpr int kSegTarget = 80;     // columns per EDT segment (warp)
+// row f3: windows per splat/reduce pass.  Each window's images are 12 B/px of scratch that
+// should stay in L2 between the splat and the reduce (with the flow gathers alongside): 4
+// windows at 1280x720 measured best (8: 63.6k, 4: 86.2k, 2: 69.0k windows/s).  IEDS_FWL_CHUNK
+// overrides it (read once per handle).
+constexpr int kFwlChunkDefault = 4;
 
 struct HostPath {
     cudaStream_t st[2] = {nullptr, nullptr};
@@ -70,10 +75,11 @@ struct ieds_handle {
     uint32_t* D2n = nullptr;   // norm_u8: [chunk][H][W] exact D2 scratch
     uint32_t* wmax = nullptr;  // norm_u8: [chunk] per-window max D2
     double* vtab = nullptr;    // norm_u8: [(W-1)^2 + (H-1)^2 + 1] fp64 transfer of every D2
-    // row f3 scratch (allocated on the first ieds_fwl_batch): kFwlChunk windows of images
-    double* fwl_Ic = nullptr;             // [kFwlChunk][H][W] fp64, zero between calls
-    int* fwl_Iu = nullptr;                // [kFwlChunk][H][W] int32, zero between calls
-    ieds::FwlPart* fwl_part = nullptr;    // [kFwlChunk][reduce blocks] per-block partial sums
+    // row f3 scratch (allocated on the first ieds_fwl_batch): fwl_chunk windows of images
+    int fwl_chunk = 0;
+    double* fwl_Ic = nullptr;             // [fwl_chunk][stride] fp64, zero between calls
+    int* fwl_Iu = nullptr;                // [fwl_chunk][stride] int32, zero between calls
+    ieds::FwlPart* fwl_part = nullptr;    // [fwl_chunk][reduce blocks] per-block partial sums
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
     uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
@@ -628,6 +634,9 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     const int red_blocks = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (stride / 4 + ieds::kFwlThreads - 1) / ieds::kFwlThreads));
     cudaError_t e = cudaSuccess;
     if (!h->fwl_Ic) {
+        h->fwl_chunk = kFwlChunkDefault;
+        if (const char* env = std::getenv("IEDS_FWL_CHUNK")) h->fwl_chunk = std::max(1, std::min(64, std::atoi(env)));
+        const int kFwlChunk = h->fwl_chunk;
         e = cudaMalloc(&h->fwl_Ic, sizeof(double) * stride * kFwlChunk);
         if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * stride * kFwlChunk);
         if (e == cudaSuccess) e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * red_blocks * kFwlChunk);
@@ -646,6 +655,7 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // splat grid: enough blocks per window to fill the GPU several times over
+    const int kFwlChunk = h->fwl_chunk;
     const int per_win = std::max(1, (4 * 148) / kFwlChunk);
     for (int c0 = 0; c0 < num_windows; c0 += kFwlChunk) {
         const int nb = std::min(kFwlChunk, num_windows - c0);

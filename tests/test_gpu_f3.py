@@ -89,7 +89,7 @@ def test_fwl_parity_hand_cases_and_degenerates():
 
 def test_fwl_parity_c3_geometry_and_chunking():
     """C3 geometry (1280x720, 75k events per window) over more windows than one scratch
-    chunk (8), so the re-zeroed scratch is reused; results do not depend on the batch."""
+    pass (4 by default), so the re-zeroed scratch is reused; results do not depend on the batch."""
     xy, t, p, off, flows, _fl, t_ref = flow_batch(GEN4, 3, 0, 10)
     g = _check(xy, t, p, off, flows, t_ref, GEN4.dt_us, GEN4.width, GEN4.height)
     # the same windows one call at a time give the same values (to the fp64 summation order)
