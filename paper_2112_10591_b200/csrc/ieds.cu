@@ -64,6 +64,7 @@ struct ieds_handle {
     int dev;
     int NW, NWP, NR, NS, SEGW;
     int band_rows, nbands;     // frame kernel: rows per CTA band, bands per window (frame_kernel.cuh)
+    int nsm;                   // SMs of the device (small batches spread a window over several)
     int chunk;        // windows per launch pair of the device path (scratch capacity)
     int host_chunk;   // windows per pipelined copy/compute step of the host path (<= chunk)
     size_t smem_frame, smem_edt, smem_edt_d2;
@@ -207,7 +208,7 @@ int window_size_for(int c) {
 
 template <int C>
 void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt) {
-    const size_t smem = ieds::window_smem_bytes(wp.H);
+    const size_t smem = ieds::window_smem_bytes(std::min(wp.H, wp.RB));
     if (fmt == IEDS_OUT_U8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
     else if (fmt == IEDS_OUT_F16) ieds::window_kernel<C, uint16_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
     else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
@@ -267,8 +268,21 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     fp.NW = h->NW;
     fp.NWP = h->NWP;
     fp.NR = h->NR;
-    fp.band_rows = h->band_rows;
-    fp.nbands = h->nbands;
+    // Small batches (latency mode, row f2): spread each window's frame over more row bands so
+    // that about two waves of CTAs run; bulk batches keep the create-time banding.
+    int band_rows = h->band_rows, nbands = h->nbands;
+    if (nb < h->nsm && h->cfg.height > 64) {
+        const int want = std::min((2 * h->nsm + nb - 1) / nb, (h->cfg.height + 31) / 32);
+        const int br = std::min(h->band_rows, ((h->cfg.height + want - 1) / want + 31) / 32 * 32);
+        if (br < band_rows) {
+            band_rows = br;
+            nbands = (h->cfg.height + br - 1) / br;
+        }
+    }
+    fp.band_rows = band_rows;
+    fp.nbands = nbands;
+    const size_t smem_frame = 4ull * ((4 + (size_t)(band_rows + 6) * h->NWP + 3) & ~3ull) +
+                              8ull * std::max(h->cfg.width, h->NWP);
     fp.n_d = h->cfg.n_d;
     fp.n_f = h->cfg.n_f;
     fp.vec_ok = ((reinterpret_cast<uintptr_t>(xy) & 15u) == 0) ? 1 : 0;
@@ -288,9 +302,9 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     cudaEvent_t pa, pb;
     prof_pair(h, 0, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
-    if (!stream_path && h->nbands > 1)   // bands OR their word rows into the column bitmap
+    if (!stream_path && nbands > 1)   // bands OR their word rows into the column bitmap
         cudaMemsetAsync(h->colmask, 0, sizeof(unsigned long long) * (size_t)nb * h->cfg.width, st);
-    ieds::frame_kernel<<<dim3(nb, h->nbands), kFrameThreads, h->smem_frame, st>>>(fp);
+    ieds::frame_kernel<<<dim3(nb, nbands), kFrameThreads, smem_frame, st>>>(fp);
     if (pb) cudaEventRecord(pb, st);
 
     if (stream_path) {
@@ -304,7 +318,15 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
         wp.K_sat = h->K_sat;
         wp.dummy = h->dummy;
         wp.one = 1u;
-        dim3 wgrid((h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps, nb);
+        // small batches: row bands (each warming its register window up over C - 1 rows
+        // above it) so that about two waves of CTAs run; bulk batches: one band
+        const int groups = (h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps;
+        int nrb = 1;
+        if (groups * nb < 2 * h->nsm) nrb = std::min((2 * h->nsm + groups * nb - 1) / (groups * nb),
+                                                   std::max(1, h->cfg.height / 32));
+        wp.RB = (h->cfg.height + nrb - 1) / nrb;
+        nrb = (h->cfg.height + wp.RB - 1) / wp.RB;
+        dim3 wgrid(groups, nb, nrb);
         prof_pair(h, 1, &pa, &pb);
         if (pa) cudaEventRecord(pa, st);
         launch_window(h->c_win, wgrid, st, wp, h->cfg.out_format);
@@ -460,6 +482,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
 
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    h->nsm = nsm;
     // Default: 8 waves of windows per launch pair (~143 MB of scratch at 1280x720), so a
     // 1000-window batch is one frame launch + one window launch with a single partial tail
     // wave instead of four launch pairs whose last one runs a mostly idle wave.  The host

@@ -41,6 +41,7 @@ struct WinParams {
     const float* __restrict__ lut;      // [K_sat + 1], lut[K_sat] = the saturated value
     uint32_t* __restrict__ dummy;       // [nb][32] sink for the lanes of a ragged strip (x >= W)
     int W, H, NW;
+    int RB;                             // rows per band (blockIdx.z); >= H: one band (the bulk path)
     int K_sat;                          // <= kWinLutMax
     uint32_t one;                       // 1 (runtime, so 0x10000 = one << 16 stays an IMAD operand)
 };
@@ -78,6 +79,7 @@ __device__ __forceinline__ void st_cs_bits(uint16_t*, uint64_t addr, uint32_t bi
 template <int C, typename OutT>
 struct WinState {
     int H, lane;
+    int ya, yb;                        // rows this CTA emits (its band)
     uint64_t op;                       // byte address of the next pixel to emit (rows in order)
     uint32_t wb;                       // row stride in bytes (0 for lanes beyond W)
     uint32_t k65536;                   // 0x10000 (runtime: the half extracts stay IMADs)
@@ -169,8 +171,8 @@ struct WinState {
         const uint32_t v = P[0];
         const uint32_t hi = __umulhi(v, k65536), lo = v - hi * 0x10000u;
         const int y0 = u - (C - 1);
-        if (y0 >= 0 && y0 < H) emit<false>(lo);
-        if (y0 + 1 >= 0 && y0 + 1 < H) emit<false>(hi);
+        if (y0 >= ya && y0 < yb) emit<false>(lo);
+        if (y0 + 1 >= ya && y0 + 1 < yb) emit<false>(hi);
     }
 
     // packed squared distances x4 from row u + R of a pair to pixels y0 + 2j, y0 + 2j + 1
@@ -188,20 +190,25 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
     const int NWP2 = p.NW + 2;
-    const int NPS = window_staged_pairs(H);
+    // this CTA's band of emitted rows [ya, yb) and the row pairs u in [u_first, u_last) it
+    // steps over: every row within C - 1 of the band (the first ones only warm the window up)
+    const int ya = blockIdx.z * p.RB, yb = min(H, ya + p.RB);
+    const int u_first = max(0, ya - (C - 1)) & ~1;
+    const int u_last = min(H + C - 1, yb + C - 1);
+    const int NPS = window_staged_pairs(min(H, p.RB));
     const uint2* pairs = reinterpret_cast<const uint2*>(wsm);
     // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
     // plus zero rows past the end, interleaved by row pair: asynchronous 4-byte copies,
     // zero-filled where out of range, all in flight at once
     {
-        const uint32_t* src = p.Edf + (size_t)b * H * NWP2 + w0;
+        const uint32_t* src = p.Edf + ((size_t)b * H + u_first) * NWP2 + w0;   // staged row 0 = row u_first
         constexpr int kRowsPerPass = (kWinWarps * 32) / kWinRowWords;   // 25 rows x 10 words
         const int c = threadIdx.x % kWinRowWords, y_first = threadIdx.x / kWinRowWords;
         const bool col_ok = w0 + c < NWP2;
         const uint32_t base = (uint32_t)__cvta_generic_to_shared(wsm);
         if (y_first < kRowsPerPass) {
             for (int y = y_first; y < 2 * NPS; y += kRowsPerPass) {
-                const bool ok = col_ok && y < H;
+                const bool ok = col_ok && u_first + y < H;
                 const uint32_t* g = ok ? src + (size_t)y * NWP2 + c : src;
                 const uint32_t dst = base + 8u * (uint32_t)((y >> 1) * kWinRowWords + c) + 4u * (uint32_t)(y & 1);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(g), "r"(ok ? 4 : 0)
@@ -226,11 +233,13 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     WinState<C, OutT> st;
     st.H = H;
     st.lane = lane;
+    st.ya = ya;
+    st.yb = yb;
     st.k65536 = p.one << 16;
     st.ksat4x2 = (4u * (uint32_t)p.K_sat) * 0x10001u;
     st.lut = lut_s;
     if (x < p.W) {
-        st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.S) + ((size_t)b * H * p.W + x));
+        st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.S) + (((size_t)b * H + ya) * p.W + x));
         st.wb = (uint32_t)(p.W * sizeof(OutT));
     } else {   // lanes of a ragged last strip write to a private sink, stride 0
         st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.dummy + 32 * (size_t)b) + lane);
@@ -238,9 +247,9 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     }
     // the unchecked rotations step only the low address word: every lane's column of this
     // window must lie inside one 4 GB-aligned range (else all rotations take the checked path)
-    const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(H - 1);
+    const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(yb - ya - 1);
     const bool fast_ok = __all_sync(0xFFFFFFFFu, (last >> 32) == (st.op >> 32));
-    const uint2* pr = pairs + warp;   // this strip's words w-1, w, w+1 of pair 0
+    const uint2* pr = pairs + warp;   // this strip's words w-1, w, w+1 of staged pair 0 (row u_first)
     constexpr uint32_t kLeft = ~0u << (33 - C);        // columns 32w-(C-1) .. 32w-1 of word w-1
     constexpr uint32_t kRight = (1u << (C - 1)) - 1u;  // columns 32w+32 .. 32w+30+C of word w+1
 
@@ -248,15 +257,15 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     uint32_t P[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) P[k] = st.ksat4x2;
-    const int total = H + C - 1;   // row pairs u = 0, 2, ... < total
-    const int npairs = (total + 1) >> 1;
-    int u = 0;
+    const int npairs = (u_last - u_first + 1) >> 1;   // staged row pairs this CTA steps over
+    auto lp = [&](int uu) { return pr + ((uu - u_first) >> 1) * kWinRowWords; };
+    int u = u_first;
     if (fast_ok) {
-        // rows y0 = u - C + 1 < 0 are not emitted: rolled steps until the first even u >= C - 1
-        for (; u < ((C - 1 + 1) & ~1) && u < total; u += 2) st.step_rolled(pr + (u >> 1) * kWinRowWords, u, P);
-        // steady state: whole rotations whose emitted rows (up to u + C) all lie in the frame
-        for (; u + C < H; u += 2 * C) {
-            const int q0 = u >> 1;
+        // rows y0 = u - C + 1 < ya are not emitted: rolled steps until the first even u >= ya + C - 1
+        for (; u < ya + C - 1 && u < u_last; u += 2) st.step_rolled(lp(u), u, P);
+        // steady state: whole rotations whose emitted rows (up to u + C) all lie in the band
+        for (; u + C < yb; u += 2 * C) {
+            const int q0 = (u - u_first) >> 1;
             // activity of the rotation's C row pairs, lane j < C testing pair q0 + j: rows 2q,
             // 2q+1 hold a set pixel in columns [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane
             // has h < C there (exactly the lanes' own test)
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
             st.template rotation<0>(pr + q0 * kWinRowWords, act, P);
         }
     }
-    for (; u < total; u += 2) st.step_rolled(pr + (u >> 1) * kWinRowWords, u, P);
+    for (; u < u_last; u += 2) st.step_rolled(lp(u), u, P);
 }
 
 }  // namespace ieds

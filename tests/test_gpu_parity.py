@@ -344,3 +344,33 @@ def test_largest_frames_create():
         bld.sync()
         assert bool((S == 1.0).all())
 
+
+
+def test_small_batch_bands_match_bulk_batch():
+    """Row f2 latency mode: a batch smaller than the GPU spreads each window over row bands
+    (frame kernel and window kernel); the same windows inside a 300-window batch use one band
+    each.  Surfaces (and, on the exact path, D2) are identical bit for bit."""
+    torch = _torch()
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 200, 300)
+    dev = torch.device("cuda", 0)
+    txy = torch.from_numpy(xy.view(np.int32)).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    pick = [0, 137, 299]
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0) as bld:
+        S_all = bld.build_batch(txy, toff)
+        D_all = torch.empty((300, c.height, c.width), dtype=torch.int32, device=dev)
+        bld.build_batch(txy, toff, sqdist=D_all)
+        for k in pick:
+            one = torch.tensor([0, int(off[k + 1] - off[k])], dtype=torch.int64, device=dev)
+            ev = txy[int(off[k]):int(off[k + 1])]
+            S1 = bld.build_batch(ev, one)
+            D1 = torch.empty((1, c.height, c.width), dtype=torch.int32, device=dev)
+            bld.build_batch(ev, one, sqdist=D1)
+            bld.sync()
+            assert torch.equal(S1[0], S_all[k]), k
+            assert torch.equal(D1[0], D_all[k]), k
+    ref = oracle.build_window(xy[off[0]:off[1]], c.width, c.height, wl.n_d, wl.n_f, a)
+    assert np.abs(S_all[0].cpu().numpy().astype(np.float64) - ref["S"]).max() <= TOL
