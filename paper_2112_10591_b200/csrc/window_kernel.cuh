@@ -34,6 +34,10 @@ constexpr int kWinRowWords = kWinWarps + 2;       // E_df words of one row a CTA
 constexpr int kWinRowBytes = 4 * kWinRowWords;
 constexpr int kWinMaxC = 31;
 constexpr int kWinLutMax = 1024;                  // K_sat bound of the window path
+#ifndef IEDS_WIN_SPLIT
+#define IEDS_WIN_SPLIT 4
+#endif
+constexpr int kSplit = IEDS_WIN_SPLIT;             // registers per step updated via the FMA pipe
 
 struct WinParams {
     const uint32_t* __restrict__ Edf;   // [nb][H][NW+2], word w of row y at 1 + w, zero guards
@@ -83,6 +87,7 @@ struct WinState {
     uint64_t op;                       // byte address of the next pixel to emit (rows in order)
     uint32_t wb;                       // row stride in bytes (0 for lanes beyond W)
     uint32_t k65536;                   // 0x10000 (runtime: the half extracts stay IMADs)
+    uint32_t one;                      // 1 (runtime: the split updates' adds stay IMADs)
     uint32_t ksat4x2;                  // 4*K_sat in both halves: the start value of every slot
     const uint32_t* lut;               // shared table, raw output bit patterns
 
@@ -128,9 +133,16 @@ struct WinState {
             for (int j = 0; j < C; ++j) {
                 const int m = (j + S + 1) % C;
                 const uint32_t prev = (j + 1 < C) ? P[m] : ksat4x2;
-                // two fused packed add+min: no carries cross the halves because every sum
-                // stays below 4 * (31^2 + 31^2) < 2^16
-                P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sq2<0>(j))), __vadd2(h2b, sq2<1>(j)));
+                if (j < kSplit) {
+                    // FMA-pipe adds (a plain 32-bit add is the packed add: no carry crosses
+                    // the halves) and one 3-way packed min on the ALU
+                    const uint32_t ta = h2a * one + sq2<0>(j), tb = h2b * one + sq2<1>(j);
+                    P[m] = __vimin3_u16x2(prev, ta, tb);
+                } else {
+                    // two fused packed add+min: no carries cross the halves because every sum
+                    // stays below 4 * (31^2 + 31^2) < 2^16
+                    P[m] = __vminu2(__vminu2(prev, __vadd2(h2a, sq2<0>(j))), __vadd2(h2b, sq2<1>(j)));
+                }
             }
         } else {
             P[S % C] = ksat4x2;   // the new last register starts empty
@@ -236,6 +248,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     st.ya = ya;
     st.yb = yb;
     st.k65536 = p.one << 16;
+    st.one = p.one;
     st.ksat4x2 = (4u * (uint32_t)p.K_sat) * 0x10001u;
     st.lut = lut_s;
     if (x < p.W) {
