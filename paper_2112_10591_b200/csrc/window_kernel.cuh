@@ -15,12 +15,14 @@
 // packed add+min (VIADDMNMX.U16x2 with an immediate) per register and row; pixel u-C+1 is
 // final after row u and is emitted with one coalesced 128-byte store per warp.  The loop is
 // unrolled over the C register phases of one rotation so every slot/distance is a
-// compile-time constant: no stack, no divergence.  The rotations in the middle of the frame
+// compile-time constant: no stack, no divergence.  (kSplit of the C registers take their two
+// adds on the FMA pipe instead, then one 3-way packed min: the kernel is co-limited by the ALU
+// pipe and by issue.)  The rotations in the middle of the frame
 // (all emitted rows inside the frame) run without any range check; only the first and the
 // last rotation carry them.  Instruction budget per row pair (2 pixels), see DESIGN.md §6:
 //   activity      uniform bit test + BRA (one ballot per rotation gives the C pair bits)
 //   active only:  h of 2 rows: 3 LDS.64 + 2 x (2 SHF + BREV + LOP3 + FLO.SH) + 4 IMAD (h^2),
-//                 2C VIADDMNMX.U16x2
+//                 2 (C - kSplit) VIADDMNMX.U16x2 + kSplit x (2 IMAD + VIMNMX3.U16x2)
 //   emit          2 IMAD extracts + 2 LDS (table) + 2 STG + 2 32-bit pointer adds
 #pragma once
 #include <cuda_fp16.h>
