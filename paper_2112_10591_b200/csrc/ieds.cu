@@ -304,7 +304,16 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     if (pa) cudaEventRecord(pa, st);
     if (!stream_path && nbands > 1)   // bands OR their word rows into the column bitmap
         cudaMemsetAsync(h->colmask, 0, sizeof(unsigned long long) * (size_t)nb * h->cfg.width, st);
-    ieds::frame_kernel<<<dim3(nb, nbands), kFrameThreads, smem_frame, st>>>(fp);
+    // Small frames: small CTAs, several per SM, so the scatter and walk phases of different
+    // windows overlap and the walk's row bands stay long (346x260, C2: the frame kernel takes
+    // 0.053 / 0.038 / 0.032 / 0.030 ms per 1184 windows at 1024 / 512 / 256 / 128 threads).
+    // Large frames (one CTA per SM by shared memory) keep 1024 threads (1280x720: 0.145 /
+    // 0.143 / 0.151 ms at 1024 / 768 / 512).  The walk needs a thread per word column.
+    const size_t fwords = (size_t)band_rows * h->NWP;
+    int fthreads = fwords <= 4096 ? 128 : fwords <= 16384 ? 256 : kFrameThreads;
+    if (const char* ev = std::getenv("IEDS_FRAME_THREADS")) fthreads = std::max(32, std::min(1024, std::atoi(ev)));
+    fthreads = std::max(fthreads, (h->NW + 31) / 32 * 32);
+    ieds::frame_kernel<<<dim3(nb, nbands), fthreads, smem_frame, st>>>(fp);
     if (pb) cudaEventRecord(pb, st);
 
     if (stream_path) {
