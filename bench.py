@@ -236,6 +236,51 @@ def run_reference(args):
     return 0
 
 
+def run_config_brief(args, name, dev, stream, world, local, peak):
+    """Another §8(d) workload (e.g. C2, 346x260) on the same device: surfaces/s and the
+    whole-path HBM fraction over a few steps, inputs resident (not the metric's config)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_10591_b200 as ieds
+
+    wl = WORKLOADS[name]
+    c = wl.scene
+    nwin = wl.n_windows
+    rank = int(os.environ.get("RANK", "0"))
+    xy, off = generate(name, rank * nwin, nwin)
+    txy = torch.from_numpy(xy.view(np.int32)).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    S = torch.empty((nwin, c.height, c.width), dtype=torch.float32, device=dev)
+    bld = ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
+    for _ in range(max(1, args.warmup)):
+        bld.build_batch(txy, toff, S)
+    ksteps = max(1, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ksteps):
+        bld.build_batch(txy, toff, S)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    bld.sync()
+    bld.close()
+    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item()) / ksteps
+    n_ev = int(off[-1])
+    bytes_step = 4.0 * n_ev + 4.0 * c.width * c.height * nwin + 8.0 * (nwin + 1)
+    del S
+    return {"workload": f"{name}: {c.width}x{c.height}, {nwin} windows x {c.events_per_window} events per GPU",
+            "value": nwin * max(1, world) / (ms / 1e3), "unit": "surfaces/s", "ms_per_step": ms, "steps": ksteps,
+            "hbm_frac_path": bytes_step / (ms / 1e3) / 1e9 / peak,
+            "note": "SURVEY §8(d) ceiling at the measured peak: 14.86 M surfaces/s"}
+
+
 def run_f4(args, dev, stream, world, local, wl):
     """Row f4: the stateful flow consumer (ieds_flow_step, reading R21) at the
     paper's HD settings (3 levels, weight 500, 20 sweeps) over the surfaces and
@@ -552,6 +597,11 @@ def run_ours(args):
         f3 = run_f3(args, dev, stream, world, local, peak)
 
     # row f4: the flow consumer on consecutive C3 surfaces
+    # the low-resolution config of SURVEY §8(d) (C2: 346x260, 10,000 windows per GPU)
+    c2 = None
+    if not args.no_c2 and args.config != "C2":
+        c2 = run_config_brief(args, "C2", dev, stream, world, local, peak)
+
     f4 = None
     if not args.no_f4:
         f4 = run_f4(args, dev, stream, world, local, wl)
@@ -643,6 +693,7 @@ def run_ours(args):
         "f2_latency": lat,
         "f3_fwl": f3,
         "f4_flow": f4,
+        "c2_lowres": c2,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -664,6 +715,7 @@ def main():
     ap.add_argument("--no-f1", action="store_true", help="skip the 8-bit surface (row f1) run")
     ap.add_argument("--no-f3", action="store_true", help="skip the FWL (row f3) run")
     ap.add_argument("--no-f4", action="store_true", help="skip the flow consumer (row f4) run")
+    ap.add_argument("--no-c2", action="store_true", help="skip the low-resolution C2 run")
     ap.add_argument("--f3-windows", type=int, default=64, help="C3-geometry windows of the FWL (row f3) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")
