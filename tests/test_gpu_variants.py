@@ -193,3 +193,29 @@ def test_u8_normalised_workload_c3_sampled():
     for b in range(3):
         ref = oracle.build_window(xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a)
         assert np.array_equal(Q[b], oracle.quantize_norm_u8(ref["D2"], "log")), b
+
+
+@pytest.mark.parametrize("out", ["u8", "f16"])
+def test_variants_bulk_batch_sampled(out):
+    """u8 / f16 in the bulk launch configuration (300 windows: one row band per window, the
+    shape bench.py times) -- sampled windows against the oracle, bit-exact."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 400, 300)
+    dev = torch.device("cuda", 0)
+    with ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=0, out=out) as bld:
+        Q = bld.build_batch(torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev))
+        bld.sync()
+    for b in (0, 151, 299):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f, a)
+        got = Q[b].cpu().numpy()
+        if out == "u8":
+            assert np.array_equal(got, oracle.quantize_u8(ref["S"])), b
+        else:
+            exp16 = ref["S"].astype(np.float16)
+            assert np.array_equal(got.view(np.uint16), exp16.view(np.uint16)), b
