@@ -219,3 +219,24 @@ def test_variants_bulk_batch_sampled(out):
         else:
             exp16 = ref["S"].astype(np.float16)
             assert np.array_equal(got.view(np.uint16), exp16.view(np.uint16)), b
+
+
+@pytest.mark.parametrize("out", ["u8", "f16"])
+def test_host_entry_point_variants_match_device(out):
+    """ieds_build_batch_host (pinned copies pipelined with the kernels over several chunks)
+    returns the same u8 / f16 surfaces as the device entry point."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    wl = WORKLOADS["C1"]
+    c = wl.scene
+    xy, off = batch_events(c, wl.seed, 30, 9)
+    dev = torch.device("cuda", 0)
+    with ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=0, out=out,
+                      chunk_windows=4) as bld:
+        Sd = bld.build_batch(torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev))
+        bld.sync()
+        Sh = bld.build_batch_host(xy, off)
+    assert Sh.dtype == {"u8": np.uint8, "f16": np.float16}[out]
+    assert np.array_equal(Sd.cpu().numpy().view(np.uint8), Sh.view(np.uint8))
