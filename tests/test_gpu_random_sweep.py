@@ -55,3 +55,53 @@ def test_random_configs(seed):
     gpu = run_gpu(xy, off, W, H, n_d, n_f, a, xy_shift=shift)
     for b in range(nwin):
         check_window(gpu, b, xy[off[b]:off[b + 1]], W, H, n_d, n_f, a)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_epilogue_variants(seed):
+    """Row f1 over random transfer x output format x geometry x d_sat, against the oracle:
+    fp32 within 2e-6 + one rounding, 8-bit codes exact (plain Eq. (1) or normalised ablation),
+    fp16 bit-exact from the table and within one fp16 ulp beyond it (Id / ln)."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    rng = np.random.default_rng(5000 + seed)
+    W, H, n_d, n_f, d_sat = _config(rng)
+    transfer = str(rng.choice(["invexp", "linear", "bounded", "log"]))
+    out = str(rng.choice(["f32", "u8", "f16"]))
+    bound = float(rng.choice([2.0, 6.0, 9.5]))
+    a = oracle.alpha_from_dsat(d_sat)
+    if out == "u8" and transfer == "invexp" and d_sat > 9.0:
+        d_sat, a = 6.0, oracle.alpha_from_dsat(6.0)   # the 8-bit Eq. (1) table must saturate by D2 = 1024
+    wins = [random_frame_events(W, H, float(rng.choice([0.002, 0.02, 0.1])), seed=seed * 7 + k) for k in range(3)]
+    wins.append(np.zeros(0, np.uint32))
+    xy, off = csr(wins)
+    dev = torch.device("cuda", 0)
+    with ieds.Builder(W, H, n_d, n_f, alpha=a, device=0, transfer=transfer, bound=bound, out=out) as bld:
+        S = bld.build_batch(torch.from_numpy(np.ascontiguousarray(xy).view(np.int32)).to(dev),
+                            torch.from_numpy(off).to(dev))
+        bld.sync()
+    S = S.cpu().numpy()
+    for b in range(len(wins)):
+        ref = oracle.build_window(xy[off[b]:off[b + 1]], W, H, n_d, n_f, a)
+        v = oracle.transfer(ref["D2"], transfer, alpha=a, bound=bound)
+        if out == "u8":
+            q = oracle.quantize_u8(v) if transfer == "invexp" else oracle.quantize_norm_u8(ref["D2"], transfer, bound=bound)
+            assert np.array_equal(S[b], q), (transfer, b)
+        elif out == "f32":
+            fin = np.isfinite(v)
+            assert np.array_equal(np.isinf(S[b]), ~fin)
+            err = np.abs(S[b][fin].astype(np.float64) - v[fin])
+            assert np.all(err <= 2e-6 + np.abs(v[fin]) * 2.0 ** -23), (transfer, b, float(err.max()))
+        else:
+            e16 = v.astype(np.float16)
+            same = S[b].view(np.uint16) == e16.view(np.uint16)
+            if transfer in ("invexp", "bounded"):
+                assert same.all(), (transfer, b)
+            else:
+                tab = (ref["D2"] >= 0) & (ref["D2"] < 1024)
+                assert same[tab].all(), (transfer, b)
+                fin = np.isfinite(e16)
+                ulp = np.spacing(np.abs(e16[fin])).astype(np.float64)
+                assert np.all(np.abs(S[b][fin].astype(np.float64) - e16[fin].astype(np.float64)) <= ulp)
