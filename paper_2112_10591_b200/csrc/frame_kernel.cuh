@@ -1,10 +1,12 @@
-// frame_kernel.cuh -- rows a1..a3 of the hot path, one CTA per window.
+// frame_kernel.cuh -- rows a1..a3 of the hot path, one CTA per window (per row band).
 //
 //   a1 scatter   events -> bit-packed edge image E in shared memory      (§III-A)
 //   a2 denoise   E_d  = E   & [n4_E   >= N_d]                            (Alg. 1)
 //   a3 fill      E_df = E_d | [n4_E_d >= N_f]                            (Alg. 2)
-//   then         E_df is transposed into column words T (bit i of T[r][x] = E_df(x, 32r+i))
-//                plus a per-column bitmap of non-empty word-rows, which is all the EDT needs.
+//   then, default path: E_df rows into the row-major scratch the window kernel reads (a2 and a3
+//                fused into one read-only walk per word column, see df_walk);
+//   exact path:  E_df transposed into column words T (bit i of T[r][x] = E_df(x, 32r+i)) plus a
+//                per-column bitmap of non-empty word-rows, which is all the exact EDT needs.
 //
 // Layout: one CTA per (window, row band).  Band k covers frame rows [ylo, yhi) =
 // [k * BR, min(H, (k + 1) * BR)) (BR = band_rows, a multiple of 32 when there are several bands;

@@ -1,9 +1,11 @@
 // ieds.cu -- C ABI (include/ieds.h) of the batched IEDS build on B200 (sm_100a).
 //
 // Host side: configuration validation, scratch ownership, the fp64-built Eq. (1) table,
-// stream-ordered launches chunk by chunk, the latched device error flag, and the
-// pipelined host-buffer entry point.  Kernels: frame_kernel.cuh (a1-a3), edt_kernel.cuh
-// (a4-a5).
+// stream-ordered launches chunk by chunk (launch shapes: row bands for large frames and for
+// small batches), the latched device error flag, and the pipelined host-buffer entry point.
+// Kernels: frame_kernel.cuh (a1-a3), window_kernel.cuh (a4-a5, default), edt_kernel.cuh
+// (a4-a5 exact everywhere), norm_kernel.cuh (row f1 normalised 8-bit), windowing_kernel.cuh
+// (row f2), fwl_kernel.cuh (row f3).  Row f4 lives in flow.cu.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
