@@ -18,6 +18,9 @@
  * transfers normalised by their frame maximum, and float16 surfaces.
  * alpha may be derived from the saturation distance with ieds_alpha_from_dsat (Eq. (2)-(3),
  * P:228-233).
+ * Further rows: on-device Delta-T windowing (ieds_window_offsets, row f2), the
+ * flow-compensated event image and Flow Warping Loss (ieds_fwl_batch, row f3), and
+ * a stateful flow consumer with the P:248 edge masking (ieds_flow_*, row f4).
  *
  * Memory model: every array argument of ieds_build_batch is a DEVICE pointer owned by the
  * caller (e.g. a torch tensor); ieds_build_batch_host takes HOST pointers.  The handle owns
