@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
     // ---- clear the frame and the column bitmap
     {
         uint4 z = make_uint4(0, 0, 0, 0);
-        uint4* f4 = reinterpret_cast<uint4*>(fr);
+        uint4* f4 = reinterpret_cast<uint4*>(smem);   // from the 4 zero words on (see Layout)
         const int n4 = (nframe + 3) >> 2;
         for (int i = tid; i < n4; i += nthr) f4[i] = z;
         if (p.T)
