@@ -676,7 +676,11 @@ def run_ours(args):
                      "traffic": traffic_per_launch(args.traffic, nwin / max(1, edt_n // args.steps)),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": edt_bytes_per_launch, "avg_launch_ms": edt_avg_ms,
-                     "share_of_step": edt_ms / max(1e-9, ms_max)},
+                     "share_of_step": edt_ms / max(1e-9, ms_max),
+                     "limiter": {"measured": "ALU pipe + issue (not DRAM)",
+                                 "evidence": "profiles/r01_ncu_full_frame_window.md: window_kernel "
+                                             "sm__pipe_alu_cycles_active ~70 %, issue ~75 %, DRAM ~45 %; "
+                                             "~24 lane-instructions per pixel (DESIGN §6)"}},
         "kernels": {"frame_kernel": {"avg_ms": fr_avg_ms, "launches": fr_n,
                                      "achieved_gbs": fr_bytes_per_launch / (fr_avg_ms / 1e3) / 1e9 if fr_avg_ms else None,
                                      "share_of_step": fr_ms / max(1e-9, ms_max)},
