@@ -92,7 +92,7 @@ typedef struct {
 #define IEDS_TRANSFER_LOG 3     /* ln(d + 1); empty -> +inf                          */
 #define IEDS_OUT_F32 0          /* float32 surfaces                                          */
 #define IEDS_OUT_U8 1           /* uint8.  Eq. (1): q = round(255 * S), half away from zero  */
-                                /* (P:231); q must saturate (255) for some D2 <= 1024.        */
+                                /* (P:231); q must saturate (255) for some D2 <= 2048.        */
                                 /* Id / min(d, bound) / ln(d+1): q = round(255 * v / vmax),   */
                                 /* vmax = the frame maximum of v; empty   */
                                 /* frame -> 255, vmax = 0 -> 0 (DESIGN reading R17).  This    */
@@ -103,7 +103,7 @@ typedef struct {
                                 /* the fp32 value rounded to nearest even)                    */
 
 /* Always run the uncapped exact-EDT kernel.  By default, when sqdist is not requested and
- * the saturation radius c = ceil(sqrt(K_sat)) is <= 31 pixels, the surface is produced by
+ * the saturation radius c = ceil(sqrt(K_sat)) is <= 40 pixels, the surface is produced by
  * the saturation-aware streaming kernel, which evaluates D2 exactly wherever D2 < K_sat and
  * gives bit-identical surfaces (K_sat = first D2 whose fp32 Eq. (1) value is 1.0f). */
 #define IEDS_FLAG_EXACT_EDT 1

@@ -199,7 +199,7 @@ void prof_pair(ieds_handle* h, int kind, cudaEvent_t* a, cudaEvent_t* b) {
 }
 
 // window sizes the branch-free kernel is instantiated for (c is rounded up: any C >= c is exact)
-constexpr int kWinSizes[] = {4, 6, 8, 10, 12, 14, 16, 19, 22, 25, 28, 31};
+constexpr int kWinSizes[] = {4, 6, 8, 10, 12, 14, 16, 19, 22, 25, 28, 31, 34, 37, 40};
 
 int window_size_for(int c) {
     for (int v : kWinSizes)
@@ -210,14 +210,15 @@ int window_size_for(int c) {
 
 template <int C>
 void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt) {
-    const size_t smem = ieds::window_smem_bytes(std::min(wp.H, wp.RB));
+    const size_t smem = ieds::window_smem_bytes(std::min(wp.H, wp.RB), C);
     if (fmt == IEDS_OUT_U8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
     else if (fmt == IEDS_OUT_F16) ieds::window_kernel<C, uint16_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
     else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
 }
 
 template <int C>
-cudaError_t window_attr_t(size_t smem) {
+cudaError_t window_attr_t(int H) {
+    const size_t smem = ieds::window_smem_bytes(H, C);
     cudaError_t e = cudaFuncSetAttribute(ieds::window_kernel<C, float>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
@@ -229,11 +230,12 @@ cudaError_t window_attr_t(size_t smem) {
     return e;
 }
 
-cudaError_t window_attrs(size_t smem) {
+cudaError_t window_attrs(int H) {
     cudaError_t e = cudaSuccess;
-#define IEDS_WIN_ATTR(c) if (e == cudaSuccess) e = window_attr_t<c>(smem);
+#define IEDS_WIN_ATTR(c) if (e == cudaSuccess) e = window_attr_t<c>(H);
     IEDS_WIN_ATTR(4) IEDS_WIN_ATTR(6) IEDS_WIN_ATTR(8) IEDS_WIN_ATTR(10) IEDS_WIN_ATTR(12) IEDS_WIN_ATTR(14)
     IEDS_WIN_ATTR(16) IEDS_WIN_ATTR(19) IEDS_WIN_ATTR(22) IEDS_WIN_ATTR(25) IEDS_WIN_ATTR(28) IEDS_WIN_ATTR(31)
+    IEDS_WIN_ATTR(34) IEDS_WIN_ATTR(37) IEDS_WIN_ATTR(40)
 #undef IEDS_WIN_ATTR
     return e;
 }
@@ -251,7 +253,10 @@ void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp,
         case 22: launch_window_t<22>(grid, st, wp, u8); break;
         case 25: launch_window_t<25>(grid, st, wp, u8); break;
         case 28: launch_window_t<28>(grid, st, wp, u8); break;
-        default: launch_window_t<31>(grid, st, wp, u8); break;
+        case 31: launch_window_t<31>(grid, st, wp, u8); break;
+        case 34: launch_window_t<34>(grid, st, wp, u8); break;
+        case 37: launch_window_t<37>(grid, st, wp, u8); break;
+        default: launch_window_t<40>(grid, st, wp, u8); break;
     }
 }
 
@@ -462,7 +467,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->c_win = window_size_for(std::max(2, h->c_sat));
     h->norm_u8 = cfg->out_format == IEDS_OUT_U8 && cfg->transfer != IEDS_TRANSFER_INVEXP;
     h->streaming = h->c_win > 0 && h->K_sat <= kLutMax && !(cfg->flags & IEDS_FLAG_EXACT_EDT) && !h->norm_u8 &&
-                   ieds::window_smem_bytes(H) <= (size_t)kMaxSmem;
+                   ieds::window_smem_bytes(H, std::max(2, h->c_win)) <= (size_t)kMaxSmem;
 
     // 4 zero words + the band's frame rows (band_rows + 6), then the column bitmap of the exact
     // path.  One band holds the whole frame whenever that fits (1280x720: 129 KB); larger
@@ -505,7 +510,7 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
-    if (e == cudaSuccess && h->streaming) e = window_attrs(ieds::window_smem_bytes(H));
+    if (e == cudaSuccess && h->streaming) e = window_attrs(H);
     if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);

@@ -32,10 +32,10 @@
 namespace ieds {
 
 constexpr int kWinWarps = 8;                      // warps (strips) per CTA
-constexpr int kWinRowWords = kWinWarps + 2;       // E_df words of one row a CTA needs (strips +- 1)
-constexpr int kWinRowBytes = 4 * kWinRowWords;
-constexpr int kWinMaxC = 31;
-constexpr int kWinLutMax = 1024;                  // K_sat bound of the window path
+constexpr int kWinMaxC = 40;                      // C <= 31: h from 1 word per side; 31 < C <= 40: 2 words
+constexpr int kWinLutMax = 2048;                  // K_sat bound of the window path
+// E_df words of one staged row: the CTA's strips plus 1 word per side (C <= 31) or 2 (C > 31)
+__host__ __device__ constexpr int window_row_words(int C) { return kWinWarps + (C > 31 ? 4 : 2); }
 #ifndef IEDS_WIN_SPLIT
 #define IEDS_WIN_SPLIT 4
 #endif
@@ -55,8 +55,10 @@ struct WinParams {
 // row pairs a CTA stages: H rows plus zero rows for the reads past H (steps read pairs
 // q < (H + C) / 2)
 __host__ __device__ constexpr int window_staged_pairs(int H) { return (H + 2 * kWinMaxC + 2) / 2; }
-// dynamic shared memory: [pairs][kWinRowWords] uint2 {row 2q, row 2q+1}
-__host__ __device__ constexpr size_t window_smem_bytes(int H) { return 8ull * window_staged_pairs(H) * kWinRowWords; }
+// dynamic shared memory: [pairs][row words] uint2 {row 2q, row 2q+1}
+__host__ __device__ constexpr size_t window_smem_bytes(int H, int C) {
+    return 8ull * window_staged_pairs(H) * window_row_words(C);
+}
 
 // squared distance x4 from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
 template <int C>
@@ -84,6 +86,10 @@ __device__ __forceinline__ void st_cs_bits(uint16_t*, uint64_t addr, uint32_t bi
 
 template <int C, typename OutT>
 struct WinState {
+    static constexpr bool WIDE = C > 31;                  // h needs a second word per side
+    static constexpr int RW = window_row_words(C);        // staged words per row
+    static constexpr int OFF = WIDE ? 2 : 1;              // this strip's word w is at index OFF
+    using ActT = typename std::conditional<(C > 32), uint64_t, uint32_t>::type;   // a bit per step
     int H, lane;
     int ya, yb;                        // rows this CTA emits (its band)
     uint64_t op;                       // byte address of the next pixel to emit (rows in order)
@@ -93,13 +99,32 @@ struct WinState {
     uint32_t ksat4x2;                  // 4*K_sat in both halves: the start value of every slot
     const uint32_t* lut;               // shared table, raw output bit patterns
 
-    // h of the row at `rp` (this strip's words w-1, w, w+1), clamped to <= 31:
+    // h of a row for this lane from its strip's words (w-1, w, w+1), clamped to <= 31:
     // clz of (columns x-31..x with x at the MSB) | bitreverse(columns x..x+31) -- the leading
     // zero count of an OR is the min of the two one-sided distances; bit 0 bounds it by 31.
     __device__ __forceinline__ uint32_t h_of(uint32_t tl, uint32_t t, uint32_t tr) const {
         const uint32_t left = __funnelshift_rc(tl, t, lane + 1);
         const uint32_t right = __funnelshift_r(t, tr, lane);
         return clz_shiftamt(left | __brev(right) | 1u);
+    }
+    // WIDE (C > 31): words w-2 .. w+2; distances 0..31 from the inner pair of words (no guard
+    // bit: an empty window reads 0xFFFFFFFF), 32..63 from the outer pair (guard bit: <= 63)
+    __device__ __forceinline__ uint32_t h_of5(uint32_t tl2, uint32_t tl, uint32_t t, uint32_t tr, uint32_t tr2) const {
+        const uint32_t near = __funnelshift_rc(tl, t, lane + 1) | __brev(__funnelshift_r(t, tr, lane));
+        const uint32_t far = __funnelshift_rc(tl2, tl, lane + 1) | __brev(__funnelshift_r(tr, tr2, lane));
+        return min(clz_shiftamt(near), 32u + clz_shiftamt(far | 1u));
+    }
+    // h of rows 2q, 2q+1 from this strip's staged words of pair q
+    __device__ __forceinline__ void h_pair(const uint2* q, uint32_t& ha, uint32_t& hb) const {
+        if constexpr (WIDE) {
+            const uint2 a = q[0], l = q[1], c = q[2], r = q[3], z = q[4];
+            ha = h_of5(a.x, l.x, c.x, r.x, z.x);
+            hb = h_of5(a.y, l.y, c.y, r.y, z.y);
+        } else {
+            const uint2 l = q[0], c = q[1], r = q[2];
+            ha = h_of(l.x, c.x, r.x);
+            hb = h_of(l.y, c.y, r.y);
+        }
     }
     // store table[idx4 / 4] at op and step op one row down; FAST: the rows left in this
     // window do not cross a 4 GB boundary, so only the low address word moves
@@ -126,10 +151,10 @@ struct WinState {
     // offsets; bit S of `act` says whether rows u, u+1 hold a site fewer than C columns from
     // the strip.  All emitted rows lie inside the frame (the caller guarantees it).
     template <int S>
-    __device__ __forceinline__ void step(const uint2* pr, uint32_t act, uint32_t (&P)[C]) {
-        if (act & (1u << S)) {   // warp-uniform: a ballot result
-            const uint2 wl = pr[S * kWinRowWords], wc = pr[S * kWinRowWords + 1], wr = pr[S * kWinRowWords + 2];
-            const uint32_t ha = h_of(wl.x, wc.x, wr.x), hb = h_of(wl.y, wc.y, wr.y);
+    __device__ __forceinline__ void step(const uint2* pr, ActT act, uint32_t (&P)[C]) {
+        if (act & (ActT(1) << S)) {   // warp-uniform: a ballot result
+            uint32_t ha, hb;
+            h_pair(pr + S * RW, ha, hb);
             const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
@@ -156,7 +181,7 @@ struct WinState {
     }
 
     template <int S>
-    __device__ __forceinline__ void rotation(const uint2* pr, uint32_t act, uint32_t (&P)[C]) {
+    __device__ __forceinline__ void rotation(const uint2* pr, ActT act, uint32_t (&P)[C]) {
         if constexpr (S < C) {
             step<S>(pr, act, P);
             rotation<S + 1>(pr, act, P);
@@ -169,8 +194,8 @@ struct WinState {
     // steps the full 64-bit address.  Its code is one step long, so the hot rotation above is
     // the only large body in the instruction cache.
     __device__ __forceinline__ void step_rolled(const uint2* pq, int u, uint32_t (&P)[C]) {
-        const uint2 wl = pq[0], wc = pq[1], wr = pq[2];
-        const uint32_t ha = h_of(wl.x, wc.x, wr.x), hb = h_of(wl.y, wc.y, wr.y);
+        uint32_t ha, hb;
+        h_pair(pq, ha, hb);
         if (__any_sync(0xFFFFFFFFu, min(ha, hb) < (uint32_t)C)) {
             const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
 #pragma unroll
@@ -198,8 +223,11 @@ struct WinState {
 
 template <int C, typename OutT>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
-    static_assert(C >= 2 && C <= kWinMaxC, "window size (h is clamped to 31)");
-    __shared__ uint32_t lut_s[kWinLutMax + 1];           // table, raw output bit patterns
+    static_assert(C >= 2 && C <= kWinMaxC, "window size (h: <= 31 from one word, <= 63 from two)");
+    static_assert(C <= 31 || C >= 34, "two-word windows start at C = 34 (the activity masks)");
+    using St = WinState<C, OutT>;
+    constexpr int kWinRowWords = St::RW;
+    __shared__ uint32_t lut_s[(C <= 31 ? 1024 : kWinLutMax) + 1];   // table, raw output bit patterns
     extern __shared__ __align__(16) uint32_t wsm[];      // row pairs of E_df words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
@@ -215,15 +243,18 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     // plus zero rows past the end, interleaved by row pair: asynchronous 4-byte copies,
     // zero-filled where out of range, all in flight at once
     {
-        const uint32_t* src = p.Edf + ((size_t)b * H + u_first) * NWP2 + w0;   // staged row 0 = row u_first
-        constexpr int kRowsPerPass = (kWinWarps * 32) / kWinRowWords;   // 25 rows x 10 words
+        // staged word c of a row = scratch index w0 - OFF + 1 + c (word w0 - OFF + c; guards at
+        // 0 and NW + 1, anything beyond the row reads 0); staged row 0 = row u_first
+        const uint32_t* src = p.Edf + ((size_t)b * H + u_first) * NWP2;
+        constexpr int kRowsPerPass = (kWinWarps * 32) / kWinRowWords;   // 25 rows x 10 words (21 x 12)
         const int c = threadIdx.x % kWinRowWords, y_first = threadIdx.x / kWinRowWords;
-        const bool col_ok = w0 + c < NWP2;
+        const int sidx = w0 - St::OFF + 1 + c;
+        const bool col_ok = sidx >= 0 && sidx < NWP2;
         const uint32_t base = (uint32_t)__cvta_generic_to_shared(wsm);
         if (y_first < kRowsPerPass) {
             for (int y = y_first; y < 2 * NPS; y += kRowsPerPass) {
                 const bool ok = col_ok && u_first + y < H;
-                const uint32_t* g = ok ? src + (size_t)y * NWP2 + c : src;
+                const uint32_t* g = ok ? src + (size_t)y * NWP2 + sidx : src;
                 const uint32_t dst = base + 8u * (uint32_t)((y >> 1) * kWinRowWords + c) + 4u * (uint32_t)(y & 1);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(g), "r"(ok ? 4 : 0)
                              : "memory");
@@ -244,7 +275,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     const int w = w0 + warp;
     if (w >= p.NW) return;
     const int x = 32 * w + lane;
-    WinState<C, OutT> st;
+    St st;
     st.H = H;
     st.lane = lane;
     st.ya = ya;
@@ -264,9 +295,12 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     // window must lie inside one 4 GB-aligned range (else all rotations take the checked path)
     const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(yb - ya - 1);
     const bool fast_ok = __all_sync(0xFFFFFFFFu, (last >> 32) == (st.op >> 32));
-    const uint2* pr = pairs + warp;   // this strip's words w-1, w, w+1 of staged pair 0 (row u_first)
-    constexpr uint32_t kLeft = ~0u << (33 - C);        // columns 32w-(C-1) .. 32w-1 of word w-1
-    constexpr uint32_t kRight = (1u << (C - 1)) - 1u;  // columns 32w+32 .. 32w+30+C of word w+1
+    const uint2* pr = pairs + warp;   // this strip's words w-OFF .. w+OFF of staged pair 0 (row u_first)
+    // columns within C-1 of the strip [32w - (C-1), 32w + 31 + (C-1)]: the outermost staged
+    // words contribute their bits nearest the strip
+    constexpr int kReach = St::WIDE ? C - 33 : C - 1;   // bits of the outermost word on each side
+    constexpr uint32_t kLeft = ~0u << (32 - kReach);
+    constexpr uint32_t kRight = (1u << kReach) - 1u;
 
     // Window of 2C pixels of this lane's column as 16-bit partial minima, two per register.
     uint32_t P[C];
@@ -284,13 +318,23 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
             // activity of the rotation's C row pairs, lane j < C testing pair q0 + j: rows 2q,
             // 2q+1 hold a set pixel in columns [32w - (C-1), 32w + 31 + (C-1)], i.e. some lane
             // has h < C there (exactly the lanes' own test)
-            uint32_t any = 0u;
-            if (lane < C && q0 + lane < npairs) {
-                const uint2* q = pr + (q0 + lane) * kWinRowWords;
-                const uint2 a = q[0], m = q[1], r = q[2];
-                any = ((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight);
+            // lanes j test pairs q0 + j (and q0 + 32 + j when C > 32)
+            auto pair_any = [&](int q) -> bool {
+                const uint2* qq = pr + q * kWinRowWords;
+                if constexpr (St::WIDE) {
+                    const uint2 a = qq[0], l = qq[1], m = qq[2], r = qq[3], z = qq[4];
+                    return (((a.x | a.y) & kLeft) | l.x | l.y | m.x | m.y | r.x | r.y | ((z.x | z.y) & kRight)) != 0u;
+                } else {
+                    const uint2 a = qq[0], m = qq[1], r = qq[2];
+                    return (((a.x | a.y) & kLeft) | m.x | m.y | ((r.x | r.y) & kRight)) != 0u;
+                }
+            };
+            const bool lo = lane < C && q0 + lane < npairs && pair_any(q0 + lane);
+            typename St::ActT act = __ballot_sync(0xFFFFFFFFu, lo);
+            if constexpr (C > 32) {
+                const bool hi = lane < C - 32 && q0 + 32 + lane < npairs && pair_any(q0 + 32 + lane);
+                act |= (uint64_t)__ballot_sync(0xFFFFFFFFu, hi) << 32;
             }
-            const uint32_t act = __ballot_sync(0xFFFFFFFFu, any != 0u);
             st.template rotation<0>(pr + q0 * kWinRowWords, act, P);
         }
     }

@@ -288,7 +288,7 @@ def _stress_windows(W, H, seed):
     return wins
 
 
-@pytest.mark.parametrize("d_sat", [1.0, 3.0, 6.0, 8.0, 9.5])
+@pytest.mark.parametrize("d_sat", [1.0, 3.0, 6.0, 8.0, 9.5, 11.0, 12.0])
 def test_streaming_surface_bit_identical_to_exact(d_sat):
     """The saturation-aware streaming kernel (default when D2 is not requested) must produce the
     same fp32 surface bits as the exact-EDT kernel, for every saturation radius it serves."""
