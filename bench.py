@@ -390,8 +390,8 @@ def run_f3(args, dev, stream, world, local, peak):
            "hbm_gbs": bytes_alg / (ms / 1e3) / 1e9, "hbm_frac": bytes_alg / (ms / 1e3) / 1e9 / peak,
            "fwl_mean": fwl_mean,
            "note": "algorithmic bytes 21 B/event (xy, t, p, flow gather); the I_comp/I_uncomp images are "
-                   "L2-resident scratch (12 B/px, 8 windows per pass), so the bound is L2 atomics + the "
-                   "image reduce, not HBM"}
+                   "L2 scratch (12 B/px, 16 windows per pass) that is never read back: sum I and sum I^2 come "
+                   "from the atomics' old values; the bound is the L2 atomic rate, not HBM"}
     if rank == 0 and not args.no_cpu_baseline:
         import time as _time
 
@@ -720,7 +720,7 @@ def main():
     ap.add_argument("--no-f3", action="store_true", help="skip the FWL (row f3) run")
     ap.add_argument("--no-f4", action="store_true", help="skip the flow consumer (row f4) run")
     ap.add_argument("--no-c2", action="store_true", help="skip the low-resolution C2 run")
-    ap.add_argument("--f3-windows", type=int, default=64, help="C3-geometry windows of the FWL (row f3) run")
+    ap.add_argument("--f3-windows", type=int, default=128, help="C3-geometry windows of the FWL (row f3) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")
     ap.add_argument("--cpu-windows", type=int, default=256,

@@ -10,8 +10,9 @@
 // order (tau = (t_ref - t)/dt; xw = x + Fx*tau; x0 = floor(xw); fx = xw - x0; weights
 // (1-fx)(1-fy), fx(1-fy), (1-fx)fy, fx*fy), so the drop/floor decisions and every weight are
 // the oracle's bit for bit; only the order of the per-pixel sums differs (fp64 atomics).
-// Both images live in a zero-initialised scratch of a few windows (L2-resident: 12 B/px), the
-// reduce pass re-zeroes it as it reads it.
+// Both images live in a zero-initialised scratch of a few windows (L2-resident: 12 B/px).  The
+// sums of I and I^2 come from the splat's atomics (each add's old value, see fwl_add), so the
+// images are never read back; a memset re-zeroes the scratch for the next windows.
 #pragma once
 #include <cstdint>
 
@@ -35,20 +36,70 @@ struct FwlParams {
     int* __restrict__ err;
 };
 
-__global__ void __launch_bounds__(kFwlThreads) fwl_splat_kernel(FwlParams p) {
+// Per-window partial sums of I_comp, I_comp^2 (fp64) and I_uncomp, I_uncomp^2 (exact int64),
+// one per splat block: part[b][blk] = {sum c, sum c^2, sum u, sum u^2}.
+struct FwlPart {
+    double c, c2;
+    long long u, u2;
+};
+
+// The warp of one event (reading R19), in the oracle's fp64 order with explicit
+// round-to-nearest operations: false if the warped position is dropped (outside [0, W-1] x
+// [0, H-1], or NaN); else the top-left corner (ix, iy) and the bilinear weights.
+struct FwlWarp {
+    int ix, iy;
+    double w00, w10, w01, w11;
+};
+
+__device__ __forceinline__ bool fwl_warp(const FwlParams& p, const float2* F, int64_t tref, int64_t i, int x, int y,
+                                         FwlWarp& o) {
+    const float2 f = __ldg(F + (size_t)y * p.W + x);
+    const double dt = (double)p.dt;
+    const double tau = __ddiv_rn((double)(tref - __ldg(p.t + i)), dt);
+    const double xw = __dadd_rn((double)x, __dmul_rn((double)f.x, tau));
+    const double yw = __dadd_rn((double)y, __dmul_rn((double)f.y, tau));
+    if (!(xw >= 0.0 && xw <= (double)(p.W - 1) && yw >= 0.0 && yw <= (double)(p.H - 1))) return false;
+    const double x0 = floor(xw), y0 = floor(yw);
+    const double fx = __dsub_rn(xw, x0), fy = __dsub_rn(yw, y0);
+    const double ax = __dsub_rn(1.0, fx), ay = __dsub_rn(1.0, fy);
+    o.ix = (int)x0;
+    o.iy = (int)y0;
+    o.w00 = __dmul_rn(ax, ay);
+    o.w10 = __dmul_rn(fx, ay);
+    o.w01 = __dmul_rn(ax, fy);
+    o.w11 = __dmul_rn(fx, fy);
+    return true;
+}
+
+// Adds v to *a and returns its contribution to the sum of squares: new^2 - old^2, with old the
+// atomic's return and new = old + v exactly as the atomic rounded it.  Over all adds to one
+// pixel these terms sum to the pixel's final value squared (telescoping), so the image is
+// never read back.  Also adds v to the plain sum.
+__device__ __forceinline__ double fwl_add(double* a, double v, double& sc) {
+    const double old = atomicAdd(a, v);
+    const double nw = __dadd_rn(old, v);
+    sc += v;
+    return __dmul_rn(__dsub_rn(nw, old), __dadd_rn(nw, old));
+}
+
+// Splat: each event adds s_e = +-1 to I_uncomp at (x, y) and s_e * weight to the four corners
+// of its warped position in I_comp; the block's threads accumulate sum I and sum I^2 of both
+// images from the atomics' old values, and write one partial per block.  (Bound by the L2
+// atomic rate: taking 2 or 4 events per thread with all their atomics in flight measured no gain.)
+__global__ void __launch_bounds__(kFwlThreads) fwl_splat_kernel(FwlParams p, FwlPart* __restrict__ part) {
     const int b = blockIdx.y;
     int64_t o0 = p.offsets[b], o1 = p.offsets[b + 1];
     if (o0 < 0 || o1 < o0 || o1 > p.n_events) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.err, 2);   // kErrOrder
-        return;
+        o0 = o1 = 0;
     }
     const int W = p.W, H = p.H;
-    const size_t npx = (size_t)W * H;
     double* Ic = p.Ic + (size_t)b * p.stride;
     int* Iu = p.Iu + (size_t)b * p.stride;
-    const float2* F = p.flow + (size_t)b * npx;
+    const float2* F = p.flow + (size_t)b * W * H;
     const int64_t tref = p.t_ref[b];
-    const double dt = (double)p.dt, xmax = (double)(W - 1), ymax = (double)(H - 1);
+    double sc = 0.0, sc2 = 0.0;
+    long long su = 0, su2 = 0;
     int bad = 0;
     for (int64_t i = o0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < o1; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t v = __ldg(p.xy + i);
@@ -57,80 +108,22 @@ __global__ void __launch_bounds__(kFwlThreads) fwl_splat_kernel(FwlParams p) {
             bad = 1;
             continue;
         }
-        const bool pos = __ldg(p.p + i) > 0;
-        const size_t q = (size_t)y * W + x;
-        atomicAdd(Iu + q, pos ? 1 : -1);
-        const float2 f = __ldg(F + q);
-        const double tau = __ddiv_rn((double)(tref - __ldg(p.t + i)), dt);
-        const double xw = __dadd_rn((double)x, __dmul_rn((double)f.x, tau));
-        const double yw = __dadd_rn((double)y, __dmul_rn((double)f.y, tau));
-        if (!(xw >= 0.0 && xw <= xmax && yw >= 0.0 && yw <= ymax)) continue;   // dropped (also NaN)
-        const double x0 = floor(xw), y0 = floor(yw);
-        const double fx = __dsub_rn(xw, x0), fy = __dsub_rn(yw, y0);
-        const double ax = __dsub_rn(1.0, fx), ay = __dsub_rn(1.0, fy);
-        const int ix = (int)x0, iy = (int)y0;
-        double* c = Ic + (size_t)iy * W + ix;
-        const double w00 = __dmul_rn(ax, ay), w10 = __dmul_rn(fx, ay), w01 = __dmul_rn(ax, fy),
-                     w11 = __dmul_rn(fx, fy);
-        atomicAdd(c, pos ? w00 : -w00);
-        if (ix + 1 < W) atomicAdd(c + 1, pos ? w10 : -w10);
-        if (iy + 1 < H) {
-            atomicAdd(c + W, pos ? w01 : -w01);
-            if (ix + 1 < W) atomicAdd(c + W + 1, pos ? w11 : -w11);
+        const int s = __ldg(p.p + i) > 0 ? 1 : -1;
+        const int old = atomicAdd(Iu + (size_t)y * W + x, s);
+        su += s;
+        su2 += 2ll * s * old + 1;   // (old + s)^2 - old^2, exact
+        FwlWarp wp;
+        if (!fwl_warp(p, F, tref, i, x, y, wp)) continue;
+        double* c = Ic + (size_t)wp.iy * W + wp.ix;
+        const bool neg = s < 0;
+        sc2 += fwl_add(c, neg ? -wp.w00 : wp.w00, sc);
+        if (wp.ix + 1 < W) sc2 += fwl_add(c + 1, neg ? -wp.w10 : wp.w10, sc);
+        if (wp.iy + 1 < H) {
+            sc2 += fwl_add(c + W, neg ? -wp.w01 : wp.w01, sc);
+            if (wp.ix + 1 < W) sc2 += fwl_add(c + W + 1, neg ? -wp.w11 : wp.w11, sc);
         }
     }
     if (bad) atomicOr(p.err, 1);   // kErrRange: dropped, latched
-}
-
-// Per-window partial sums of I_comp, I_comp^2 (fp64) and I_uncomp, I_uncomp^2 (exact int64),
-// one partial per block: part[b][blk] = {sum c, sum c^2, sum u, sum u^2}; re-zeroes both
-// images.  Each window's scratch image has a stride that is a multiple of 4 pixels (the pad
-// stays zero), so a thread takes 4 pixels with two 16-byte fp64 loads and one 16-byte int32
-// load, all in flight at once.  With comp_out (tests), a plain per-pixel loop also copies
-// I_comp out.
-struct FwlPart {
-    double c, c2;
-    long long u, u2;
-};
-
-__global__ void __launch_bounds__(kFwlThreads) fwl_reduce_kernel(double* __restrict__ Ic, int* __restrict__ Iu,
-                                                                  int64_t npx, int64_t stride,
-                                                                  FwlPart* __restrict__ part, int nblk,
-                                                                  double* __restrict__ comp_out) {
-    const int b = blockIdx.y;
-    double* c = Ic + (size_t)b * stride;
-    int* u = Iu + (size_t)b * stride;
-    double sc = 0.0, sc2 = 0.0;
-    long long su = 0, su2 = 0;
-    if (comp_out) {
-        double* co = comp_out + (size_t)b * npx;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
-            const double cv = c[i];
-            const long long uv = u[i];
-            sc += cv;
-            sc2 = fma(cv, cv, sc2);
-            su += uv;
-            su2 += uv * uv;
-            co[i] = cv;
-            c[i] = 0.0;
-            u[i] = 0;
-        }
-    } else {
-        double2* c2 = reinterpret_cast<double2*>(c);
-        int4* u4 = reinterpret_cast<int4*>(u);
-        const int64_t n4 = stride >> 2;
-        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
-            const double2 a = __ldcg(c2 + 2 * j), d = __ldcg(c2 + 2 * j + 1);
-            const int4 w = __ldcg(u4 + j);
-            sc += (a.x + a.y) + (d.x + d.y);
-            sc2 = fma(a.x, a.x, fma(a.y, a.y, fma(d.x, d.x, fma(d.y, d.y, sc2))));
-            su += (long long)w.x + w.y + w.z + w.w;
-            su2 += (long long)w.x * w.x + (long long)w.y * w.y + (long long)w.z * w.z + (long long)w.w * w.w;
-            c2[2 * j] = make_double2(0.0, 0.0);
-            c2[2 * j + 1] = make_double2(0.0, 0.0);
-            u4[j] = make_int4(0, 0, 0, 0);
-        }
-    }
     for (int o = 16; o > 0; o >>= 1) {
         sc += __shfl_xor_sync(0xFFFFFFFFu, sc, o);
         sc2 += __shfl_xor_sync(0xFFFFFFFFu, sc2, o);
@@ -149,7 +142,7 @@ __global__ void __launch_bounds__(kFwlThreads) fwl_reduce_kernel(double* __restr
             t.u += s_p[k].u;
             t.u2 += s_p[k].u2;
         }
-        part[(size_t)b * nblk + blockIdx.x] = t;
+        part[(size_t)b * gridDim.x + blockIdx.x] = t;
     }
 }
 

@@ -35,11 +35,11 @@ constexpr int kFrameThreads = 1024;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
 constexpr int kLutMax = ieds::kWinLutMax;
 constexpr int kSegTarget = 80;     // columns per EDT segment (warp)
-// row f3: windows per splat/reduce pass.  Each window's images are 12 B/px of scratch that
-// should stay in L2 between the splat and the reduce (with the flow gathers alongside): 4
-// windows at 1280x720 measured best (8: 63.6k, 4: 86.2k, 2: 69.0k windows/s).  IEDS_FWL_CHUNK
-// overrides it (read once per handle).
-constexpr int kFwlChunkDefault = 4;
+// row f3: windows per splat pass.  Each window's images are 12 B/px of scratch, hit by the
+// splat's atomics and then re-zeroed by a memset; 16 windows at 1280x720 measured best
+// (4: 118k, 8: 141k, 16: 146k, 32: 131k windows/s; 64 spills far out of L2: 63k).
+// IEDS_FWL_CHUNK overrides it (read once per handle).
+constexpr int kFwlChunkDefault = 16;
 
 struct HostPath {
     cudaStream_t st[2] = {nullptr, nullptr};
@@ -657,6 +657,9 @@ int ieds_sync(ieds_handle* h, void* stream) {
     return IEDS_OK;
 }
 
+// row f3: splat blocks per window (one partial each) when `chunk` windows share a launch
+static int fwl_splat_blocks(int chunk) { return std::max(1, (4 * 148) / chunk); }
+
 int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* events_t_us, const int8_t* events_p,
                    const int64_t* window_offsets, int64_t n_events, int32_t num_windows, const float* flow,
                    const int64_t* t_ref_us, int64_t dt_us, double* fwl, double* var_comp, double* var_uncomp,
@@ -670,7 +673,6 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     const int W = h->cfg.width, H = h->cfg.height;
     const int64_t npx = (int64_t)W * H;
     const int64_t stride = (npx + 3) & ~3ll;   // 16-byte aligned window images in the scratch
-    const int red_blocks = (int)std::min<int64_t>(4096, std::max<int64_t>(1, (stride / 4 + ieds::kFwlThreads - 1) / ieds::kFwlThreads));
     cudaError_t e = cudaSuccess;
     if (!h->fwl_Ic) {
         h->fwl_chunk = kFwlChunkDefault;
@@ -678,7 +680,7 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
         const int kFwlChunk = h->fwl_chunk;
         e = cudaMalloc(&h->fwl_Ic, sizeof(double) * stride * kFwlChunk);
         if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * stride * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * red_blocks * kFwlChunk);
+        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * fwl_splat_blocks(kFwlChunk) * kFwlChunk);
         if (e == cudaSuccess) e = cudaMemset(h->fwl_Ic, 0, sizeof(double) * stride * kFwlChunk);
         if (e == cudaSuccess) e = cudaMemset(h->fwl_Iu, 0, sizeof(int) * stride * kFwlChunk);
         if (e != cudaSuccess) {
@@ -695,7 +697,7 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // splat grid: enough blocks per window to fill the GPU several times over
     const int kFwlChunk = h->fwl_chunk;
-    const int per_win = std::max(1, (4 * 148) / kFwlChunk);
+    const int per_win = fwl_splat_blocks(kFwlChunk);
     for (int c0 = 0; c0 < num_windows; c0 += kFwlChunk) {
         const int nb = std::min(kFwlChunk, num_windows - c0);
         ieds::FwlParams fp;
@@ -713,11 +715,13 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
         fp.Ic = h->fwl_Ic;
         fp.Iu = h->fwl_Iu;
         fp.err = h->err;
-        ieds::fwl_splat_kernel<<<dim3(per_win, nb), ieds::kFwlThreads, 0, st>>>(fp);
-        ieds::fwl_reduce_kernel<<<dim3(red_blocks, nb), ieds::kFwlThreads, 0, st>>>(
-            h->fwl_Ic, h->fwl_Iu, npx, stride, h->fwl_part, red_blocks,
-            comp_image ? comp_image + (size_t)c0 * npx : nullptr);
-        ieds::fwl_finalize_kernel<<<nb, ieds::kFwlThreads, 0, st>>>(h->fwl_part, red_blocks, npx, fwl + c0,
+        ieds::fwl_splat_kernel<<<dim3(per_win, nb), ieds::kFwlThreads, 0, st>>>(fp, h->fwl_part);
+        if (comp_image)
+            cudaMemcpy2DAsync(comp_image + (size_t)c0 * npx, sizeof(double) * npx, h->fwl_Ic, sizeof(double) * stride,
+                              sizeof(double) * npx, nb, cudaMemcpyDeviceToDevice, st);
+        cudaMemsetAsync(h->fwl_Ic, 0, sizeof(double) * stride * nb, st);   // zero for the next windows
+        cudaMemsetAsync(h->fwl_Iu, 0, sizeof(int) * stride * nb, st);
+        ieds::fwl_finalize_kernel<<<nb, ieds::kFwlThreads, 0, st>>>(h->fwl_part, per_win, npx, fwl + c0,
                                                                      var_comp ? var_comp + c0 : nullptr,
                                                                      var_uncomp ? var_uncomp + c0 : nullptr);
     }
