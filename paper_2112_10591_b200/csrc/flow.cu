@@ -11,10 +11,11 @@
 //   F_l    = (1 - gamma) w + gamma Pt_l ;  P_l <- F_l
 //   output = F_0, restricted to the denoised edge pixels E_d when given.
 //
-// fp32 throughout (the oracle is fp64; DESIGN states the tolerance).  One step is ~3 launches
-// from the host: the level-0 scale (reads the caller's surface), one CUDA graph with every
-// per-level kernel (captured once per pyramid parity, replayed each window), and the output /
-// masking pass (writes the caller's buffers).
+// fp32 throughout (the oracle is fp64; DESIGN states the tolerance).  Per level: one prep pass
+// (transport, upsample, warp), one gradient pass, then the sweeps 4 at a time on shared-memory
+// halo tiles with the temporal filter in the last launch's epilogue.  One step is 3 launches from the host: the level-0 scale (reads the caller's
+// surface), one CUDA graph with every per-level kernel (captured once per pyramid parity,
+// replayed each window), and the output / masking pass (writes the caller's buffers).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -67,29 +68,31 @@ __global__ void down_kernel(const float* __restrict__ src, int Ws, float* __rest
     dst[p] = (a[0] + a[1] + a[Ws] + a[Ws + 1]) * 0.25f;
 }
 
-__global__ void advect_kernel(const float2* __restrict__ P, float2* __restrict__ Pt, int W, int H) {
+// The per-level inputs of the sweeps, one pass per pixel:
+//   Pt   = P_l(p - P_l(p))                        (the previous flow transported by itself)
+//   init = Pt (coarsest level) | 2 * bilinear upsample of the coarser level's new flow
+//   J1   = J_prev,l sampled at p - init(p)       (border-clamped bilinear)
+__global__ void prep_kernel(const float2* __restrict__ P, const float2* __restrict__ Fc, int Wc, int Hc,
+                            const float* __restrict__ Jprev, float2* __restrict__ Pt, float2* __restrict__ init,
+                            float* __restrict__ J1, int W, int H) {
     IEDS_PIX(W, H)
     const float2 f = P[p];
-    Pt[p] = bl2(P, W, H, (float)x - f.x, (float)y - f.y);
+    const float2 pt = bl2(P, W, H, (float)x - f.x, (float)y - f.y);
+    Pt[p] = pt;
+    float2 in = pt;
+    if (Fc) {
+        const float2 v = bl2(Fc, Wc, Hc, ((float)x + 0.5f) * 0.5f - 0.5f, ((float)y + 0.5f) * 0.5f - 0.5f);
+        in = make_float2(2.f * v.x, 2.f * v.y);
+    }
+    init[p] = in;
+    J1[p] = bl1(Jprev, W, H, (float)x - in.x, (float)y - in.y);
 }
 
-__global__ void upsample_kernel(const float2* __restrict__ Fc, int Wc, int Hc, float2* __restrict__ F, int W, int H) {
-    IEDS_PIX(W, H)
-    const float2 v = bl2(Fc, Wc, Hc, ((float)x + 0.5f) * 0.5f - 0.5f, ((float)y + 0.5f) * 0.5f - 0.5f);
-    F[p] = make_float2(2.f * v.x, 2.f * v.y);
-}
-
-__global__ void warp_kernel(const float* __restrict__ J, const float2* __restrict__ init, float* __restrict__ J1, int W,
-                            int H) {
-    IEDS_PIX(W, H)
-    const float2 f = init[p];
-    J1[p] = bl1(J, W, H, (float)x - f.x, (float)y - f.y);
-}
-
-// G = (Ix, Iy, It, 1 / (lambda + Ix^2 + Iy^2)) -- 0 where the denominator is 0 (w = wbar there)
-__global__ void grad_kernel(const float* __restrict__ J1, const float* __restrict__ Jc, float4* __restrict__ G, int W,
-                            int H, float lam) {
-    IEDS_PIX(W, H)
+// G = (Ix, Iy, It, 1 / (lambda + Ix^2 + Iy^2)) at pixel (x, y): central differences of J1
+// (one-sided on the border), It = Jc - J1; the last entry is 0 where the denominator is 0
+// (w = wbar there)
+__device__ __forceinline__ float4 flow_grad(const float* __restrict__ J1, const float* __restrict__ Jc, size_t p, int x,
+                                            int y, int W, int H, float lam) {
     float ix, iy;
     if (W == 1) ix = 0.f;
     else if (x == 0) ix = J1[p + 1] - J1[p];
@@ -100,19 +103,108 @@ __global__ void grad_kernel(const float* __restrict__ J1, const float* __restric
     else if (y == H - 1) iy = J1[p] - J1[p - W];
     else iy = (J1[p + W] - J1[p - W]) * 0.5f;
     const float den = lam + ix * ix + iy * iy;
-    G[p] = make_float4(ix, iy, Jc[p] - J1[p], den > 0.f ? 1.f / den : 0.f);
+    return make_float4(ix, iy, Jc[p] - J1[p], den > 0.f ? 1.f / den : 0.f);
 }
 
-__global__ void jacobi_kernel(const float2* __restrict__ win, float2* __restrict__ wout, const float2* __restrict__ init,
-                              const float4* __restrict__ G, int W, int H) {
+__global__ void grad_kernel(const float* __restrict__ J1, const float* __restrict__ Jc, float4* __restrict__ G, int W,
+                            int H, float lam) {
     IEDS_PIX(W, H)
-    const float2 l = win[x > 0 ? p - 1 : p], r = win[x < W - 1 ? p + 1 : p];
-    const float2 u = win[y > 0 ? p - W : p], d = win[y < H - 1 ? p + W : p];
-    const float mx = (l.x + r.x + u.x + d.x) * 0.25f, my = (l.y + r.y + u.y + d.y) * 0.25f;
-    const float4 g = G[p];
-    const float2 i0 = init[p];
-    const float res = g.x * (mx - i0.x) + g.y * (my - i0.y) + g.z;
-    wout[p] = make_float2(mx - g.x * res * g.w, my - g.y * res * g.w);
+    G[p] = flow_grad(J1, Jc, p, x, y, W, H, lam);
+}
+
+// K Jacobi sweeps in one launch (temporal blocking): a CTA loads its tile plus a K-pixel halo
+// of w into shared memory (G and init of its cells stay in registers), runs K sweeps on a
+// shrinking region and writes the tile.  After sweep s every cell at least s cells inside the
+// region is exact, so the tile (K inside) equals K plain sweeps over the whole level, operation
+// for operation: the same clamped (replicate) border neighbours and the same fp32 expressions:
+//   w <- wbar - g (g . (wbar - init) + It) / (lambda + |g|^2),  G = (Ix, Iy, It, 1/(lambda + |g|^2)).
+// Region of 64 x 32 cells per CTA (threads 32 x 8; a thread owns columns tx, tx + 32 and rows
+// ty + 8j, j < 4), tile = region minus K on every side.
+constexpr int kTbRX = 64, kTbRY = 32, kTbThreads = 256, kTbMaxK = 4;
+
+struct TbParams {
+    const float2* win;     // w before these sweeps (init for the first launch)
+    float2* wout;          // w after them, or with blend: F = (1 - gamma) w + gamma Pt
+    const float2* init;
+    const float4* G;       // (Ix, Iy, It, 1 / (lambda + Ix^2 + Iy^2)) per pixel
+    const float2* Pt;      // with blend: the transported previous flow
+    float gamma;
+    int W, H;
+    int blend;             // last launch of the level: write F into the level's flow state
+};
+
+template <int K>
+__global__ void __launch_bounds__(kTbThreads) jacobi_tb_kernel(TbParams q) {
+    const int W = q.W, H = q.H;
+    constexpr int TX = kTbRX - 2 * K, TY = kTbRY - 2 * K;
+    __shared__ float2 sw[2][kTbRY][kTbRX];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int x0 = blockIdx.x * TX - K, y0 = blockIdx.y * TY - K;
+    float4 g[2][4];
+    float2 i0[2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int rx = tx + 32 * a, ry = ty + 8 * j, gx = x0 + rx, gy = y0 + ry;
+            if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+                const size_t p = (size_t)gy * W + gx;
+                sw[0][ry][rx] = q.win[p];
+                g[a][j] = q.G[p];
+                i0[a][j] = q.init[p];
+            }
+        }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const float2(*src)[kTbRX] = sw[s & 1];
+        float2(*dst)[kTbRX] = sw[(s + 1) & 1];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int rx = tx + 32 * a, ry = ty + 8 * j, gx = x0 + rx, gy = y0 + ry;
+                if (rx <= s || rx >= kTbRX - 1 - s || ry <= s || ry >= kTbRY - 1 - s) continue;   // not exact
+                if (gx < 0 || gx >= W || gy < 0 || gy >= H) continue;
+                const float2 l = src[ry][gx > 0 ? rx - 1 : rx], r = src[ry][gx < W - 1 ? rx + 1 : rx];
+                const float2 u = src[gy > 0 ? ry - 1 : ry][rx], d = src[gy < H - 1 ? ry + 1 : ry][rx];
+                const float mx = (l.x + r.x + u.x + d.x) * 0.25f, my = (l.y + r.y + u.y + d.y) * 0.25f;
+                const float4 gg = g[a][j];
+                const float res = gg.x * (mx - i0[a][j].x) + gg.y * (my - i0[a][j].y) + gg.z;
+                dst[ry][rx] = make_float2(mx - gg.x * res * gg.w, my - gg.y * res * gg.w);
+            }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int rx = tx + 32 * a, ry = ty + 8 * j, gx = x0 + rx, gy = y0 + ry;
+            if (rx < K || rx >= K + TX || ry < K || ry >= K + TY || gx >= W || gy >= H) continue;
+            const size_t p = (size_t)gy * W + gx;
+            const float2 w = sw[K & 1][ry][rx];
+            if (q.blend) {
+                const float2 b = q.Pt[p];
+                q.wout[p] = make_float2((1.f - q.gamma) * w.x + q.gamma * b.x, (1.f - q.gamma) * w.y + q.gamma * b.y);
+            } else {
+                q.wout[p] = w;
+            }
+        }
+}
+
+template <int K>
+void jacobi_tb(const TbParams& q, cudaStream_t st) {
+    constexpr int TX = kTbRX - 2 * K, TY = kTbRY - 2 * K;
+    jacobi_tb_kernel<K><<<dim3((q.W + TX - 1) / TX, (q.H + TY - 1) / TY), kTbThreads, 0, st>>>(q);
+}
+
+void jacobi_sweeps(int k, const TbParams& q, cudaStream_t st) {
+    switch (k) {
+        case 1: jacobi_tb<1>(q, st); break;
+        case 2: jacobi_tb<2>(q, st); break;
+        case 3: jacobi_tb<3>(q, st); break;
+        default: jacobi_tb<4>(q, st); break;
+    }
 }
 
 __global__ void blend_kernel(const float2* __restrict__ w, const float2* __restrict__ Pt, float2* __restrict__ F,
@@ -177,25 +269,37 @@ void enqueue_levels(ieds_flow_handle* h, int c, cudaStream_t st) {
                                                                h->Ws[l], h->Hs[l]);
     for (int l = h->L - 1; l >= 0; --l) {
         const int W = h->Ws[l], H = h->Hs[l];
-        const dim3 g = pgrid(W, H);
         float2* Pl = h->P + h->off[l];
-        advect_kernel<<<g, kFT, 0, st>>>(Pl, h->Pt, W, H);
-        const float2* init = h->Pt;
-        if (l < h->L - 1) {
-            upsample_kernel<<<g, kFT, 0, st>>>(h->P + h->off[l + 1], h->Ws[l + 1], h->Hs[l + 1], h->init, W, H);
-            init = h->init;
+        const bool coarsest = l == h->L - 1;
+        prep_kernel<<<pgrid(W, H), kFT, 0, st>>>(Pl, coarsest ? nullptr : h->P + h->off[l + 1],
+                                                 coarsest ? 0 : h->Ws[l + 1], coarsest ? 0 : h->Hs[l + 1],
+                                                 prev + h->off[l], h->Pt, h->init, h->J1, W, H);
+        // K sweeps from w^0 = init, kTbMaxK per launch ping-ponging w0 / w1; the last launch
+        // writes F_l = (1 - gamma) w + gamma Pt_l into the state
+        const int K = h->cfg.iterations[l];
+        if (K == 0) {   // no sweeps: F = the filter of init and Pt (w = init)
+            const int64_t n = (int64_t)W * H;
+            blend_kernel<<<(unsigned)((n + kFT - 1) / kFT), kFT, 0, st>>>(h->init, h->Pt, Pl, n, (float)h->cfg.gamma);
+            continue;
         }
-        warp_kernel<<<g, kFT, 0, st>>>(prev + h->off[l], init, h->J1, W, H);
-        grad_kernel<<<g, kFT, 0, st>>>(h->J1, cur + h->off[l], h->G, W, H, (float)h->cfg.lambda[l]);
-        // w^0 = init, then K sweeps ping-ponging w0/w1
-        cudaMemcpyAsync(h->w0, init, sizeof(float2) * (size_t)W * H, cudaMemcpyDeviceToDevice, st);
-        float2 *a = h->w0, *b = h->w1;
-        for (int k = 0; k < h->cfg.iterations[l]; ++k) {
-            jacobi_kernel<<<g, kFT, 0, st>>>(a, b, init, h->G, W, H);
-            std::swap(a, b);
+        grad_kernel<<<pgrid(W, H), kFT, 0, st>>>(h->J1, cur + h->off[l], h->G, W, H, (float)h->cfg.lambda[l]);
+        TbParams q;
+        q.init = h->init;
+        q.G = h->G;
+        q.Pt = h->Pt;
+        q.gamma = (float)h->cfg.gamma;
+        q.W = W;
+        q.H = H;
+        const float2* a = h->init;
+        for (int k = 0; k < K; k += kTbMaxK) {
+            const bool last = k + kTbMaxK >= K;
+            float2* b = last ? Pl : (a == h->w0 ? h->w1 : h->w0);
+            q.win = a;
+            q.wout = b;
+            q.blend = last ? 1 : 0;
+            jacobi_sweeps(std::min(kTbMaxK, K - k), q, st);
+            a = b;
         }
-        const int64_t n = (int64_t)W * H;
-        blend_kernel<<<(unsigned)((n + kFT - 1) / kFT), kFT, 0, st>>>(a, h->Pt, Pl, n, (float)h->cfg.gamma);
     }
 }
 
@@ -337,7 +441,8 @@ int ieds_flow_step(ieds_flow_handle* h, const float* surface, const uint32_t* ed
 int64_t ieds_flow_launches_per_step(const ieds_flow_handle* h) {
     if (!h) return 0;
     int64_t n = 2 + (h->L - 1);   // scale, down kernels, output
-    for (int l = 0; l < h->L; ++l) n += 5 + h->cfg.iterations[l] - (l == h->L - 1 ? 1 : 0);
+    for (int l = 0; l < h->L; ++l)   // prep, then grad + the sweeps (the last one blends), or a blend alone
+        n += h->cfg.iterations[l] > 0 ? 2 + (h->cfg.iterations[l] + kTbMaxK - 1) / kTbMaxK : 2;
     return n;
 }
 

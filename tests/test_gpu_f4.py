@@ -32,15 +32,15 @@ def _bits(E):
     return words
 
 
-def _run(seq, W, H, levels=3, use_mask=True):
+def _run(seq, W, H, levels=3, use_mask=True, iters=(20, 20, 20)):
     import torch
 
     import paper_2112_10591_b200 as ieds
 
     dev = torch.device("cuda", 0)
-    fo = oracle.FlowOracle(W, H, levels=levels)
+    fo = oracle.FlowOracle(W, H, levels=levels, iters=iters)
     out = []
-    with ieds.FlowEstimator(W, H, levels=levels, device=0) as fe:
+    with ieds.FlowEstimator(W, H, levels=levels, iterations=iters, device=0) as fe:
         for S, E in seq:
             S32 = S.astype(np.float32)
             Fo = fo.step(S32.astype(np.float64))
@@ -67,6 +67,20 @@ def test_flow_sequence_parity(W, H, v, levels):
         diffs.append(d)
     d = np.stack(diffs)
     assert d.mean() <= 1e-4 and d.max() <= 5e-2, (d.mean(), d.max())
+
+
+@pytest.mark.parametrize("iters", [(7, 5, 3), (1, 0, 2), (13, 9, 6)])
+def test_flow_sweep_counts(iters):
+    """The Jacobi sweeps run up to 4 per launch on halo tiles (temporal blocking); sweep counts
+    that are not multiples of 4, a single sweep and none at all match the oracle's plain
+    per-sweep iteration.  Frames of 200 x 136 leave ragged 64 x 16 tiles on every level."""
+    W, H = 200, 136
+    res = _run(_seq(W, H, 2, 6), W, H, 3, iters=iters)
+    for k, (Fo, Fg, vg, E) in enumerate(res[1:], start=1):
+        Fom, vo = oracle.mask_flow(Fo, E.astype(np.uint8))
+        assert np.array_equal(vg, vo), k
+        d = np.abs(Fg - Fom)
+        assert d.max() <= 2e-3, (iters, k, d.max())
 
 
 def test_flow_static_scene_and_dense_output():
