@@ -75,6 +75,7 @@ struct ieds_handle {
     bool streaming;            // saturation-aware window kernel usable (K_sat <= 1024)
     bool norm_u8;              // 8-bit view of Id / min / ln normalised by the frame maximum
     bool exact_ok;             // the exact-EDT kernel fits this width (sqdist requests need it)
+    bool win_packed = false;   // window kernel CTAs take strips of several windows (narrow frames)
     uint32_t* D2n = nullptr;   // norm_u8: [chunk][H][W] exact D2 scratch
     uint32_t* wmax = nullptr;  // norm_u8: [chunk] per-window max D2
     double* vtab = nullptr;    // norm_u8: [(W-1)^2 + (H-1)^2 + 1] fp64 transfer of every D2
@@ -208,31 +209,48 @@ int window_size_for(int c) {
 }
 
 
-template <int C>
-void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt) {
-    const size_t smem = ieds::window_smem_bytes(std::min(wp.H, wp.RB), C);
-    if (fmt == IEDS_OUT_U8) ieds::window_kernel<C, uint8_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
-    else if (fmt == IEDS_OUT_F16) ieds::window_kernel<C, uint16_t><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
-    else ieds::window_kernel<C, float><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+template <int C, bool PK>
+void launch_window_pk(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt) {
+    const size_t smem = ieds::window_smem_bytes(std::min(wp.H, wp.RB), C, PK);
+    if (fmt == IEDS_OUT_U8) ieds::window_kernel<C, uint8_t, PK><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+    else if (fmt == IEDS_OUT_F16) ieds::window_kernel<C, uint16_t, PK><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+    else ieds::window_kernel<C, float, PK><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
 }
 
+// packed CTAs (see window_kernel.cuh) exist for the one-word-per-side sizes C <= 31
 template <int C>
-cudaError_t window_attr_t(int H) {
-    const size_t smem = ieds::window_smem_bytes(H, C);
-    cudaError_t e = cudaFuncSetAttribute(ieds::window_kernel<C, float>,
+void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt, bool packed) {
+    if constexpr (C <= 31) {
+        if (packed) return launch_window_pk<C, true>(grid, st, wp, fmt);
+    }
+    launch_window_pk<C, false>(grid, st, wp, fmt);
+}
+
+template <int C, bool PK>
+cudaError_t window_attr_pk(int H) {
+    const size_t smem = ieds::window_smem_bytes(H, C, PK);
+    cudaError_t e = cudaFuncSetAttribute(ieds::window_kernel<C, float, PK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ieds::window_kernel<C, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(ieds::window_kernel<C, uint8_t, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ieds::window_kernel<C, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(ieds::window_kernel<C, uint16_t, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
     return e;
 }
 
-cudaError_t window_attrs(int H) {
+template <int C>
+cudaError_t window_attr_t(int H, bool packed) {
+    if constexpr (C <= 31) {
+        if (packed) return window_attr_pk<C, true>(H);
+    }
+    return window_attr_pk<C, false>(H);
+}
+
+cudaError_t window_attrs(int H, bool packed) {
     cudaError_t e = cudaSuccess;
-#define IEDS_WIN_ATTR(c) if (e == cudaSuccess) e = window_attr_t<c>(H);
+#define IEDS_WIN_ATTR(c) if (e == cudaSuccess) e = window_attr_t<c>(H, packed);
     IEDS_WIN_ATTR(4) IEDS_WIN_ATTR(6) IEDS_WIN_ATTR(8) IEDS_WIN_ATTR(10) IEDS_WIN_ATTR(12) IEDS_WIN_ATTR(14)
     IEDS_WIN_ATTR(16) IEDS_WIN_ATTR(19) IEDS_WIN_ATTR(22) IEDS_WIN_ATTR(25) IEDS_WIN_ATTR(28) IEDS_WIN_ATTR(31)
     IEDS_WIN_ATTR(34) IEDS_WIN_ATTR(37) IEDS_WIN_ATTR(40)
@@ -240,23 +258,23 @@ cudaError_t window_attrs(int H) {
     return e;
 }
 
-void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int u8) {
+void launch_window(int C, dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int u8, bool packed) {
     switch (C) {
-        case 4: launch_window_t<4>(grid, st, wp, u8); break;
-        case 6: launch_window_t<6>(grid, st, wp, u8); break;
-        case 8: launch_window_t<8>(grid, st, wp, u8); break;
-        case 10: launch_window_t<10>(grid, st, wp, u8); break;
-        case 12: launch_window_t<12>(grid, st, wp, u8); break;
-        case 14: launch_window_t<14>(grid, st, wp, u8); break;
-        case 16: launch_window_t<16>(grid, st, wp, u8); break;
-        case 19: launch_window_t<19>(grid, st, wp, u8); break;
-        case 22: launch_window_t<22>(grid, st, wp, u8); break;
-        case 25: launch_window_t<25>(grid, st, wp, u8); break;
-        case 28: launch_window_t<28>(grid, st, wp, u8); break;
-        case 31: launch_window_t<31>(grid, st, wp, u8); break;
-        case 34: launch_window_t<34>(grid, st, wp, u8); break;
-        case 37: launch_window_t<37>(grid, st, wp, u8); break;
-        default: launch_window_t<40>(grid, st, wp, u8); break;
+        case 4: launch_window_t<4>(grid, st, wp, u8, packed); break;
+        case 6: launch_window_t<6>(grid, st, wp, u8, packed); break;
+        case 8: launch_window_t<8>(grid, st, wp, u8, packed); break;
+        case 10: launch_window_t<10>(grid, st, wp, u8, packed); break;
+        case 12: launch_window_t<12>(grid, st, wp, u8, packed); break;
+        case 14: launch_window_t<14>(grid, st, wp, u8, packed); break;
+        case 16: launch_window_t<16>(grid, st, wp, u8, packed); break;
+        case 19: launch_window_t<19>(grid, st, wp, u8, packed); break;
+        case 22: launch_window_t<22>(grid, st, wp, u8, packed); break;
+        case 25: launch_window_t<25>(grid, st, wp, u8, packed); break;
+        case 28: launch_window_t<28>(grid, st, wp, u8, packed); break;
+        case 31: launch_window_t<31>(grid, st, wp, u8, packed); break;
+        case 34: launch_window_t<34>(grid, st, wp, u8, packed); break;
+        case 37: launch_window_t<37>(grid, st, wp, u8, packed); break;
+        default: launch_window_t<40>(grid, st, wp, u8, packed); break;
     }
 }
 
@@ -336,16 +354,18 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
         wp.one = 1u;
         // small batches: row bands (each warming its register window up over C - 1 rows
         // above it) so that about two waves of CTAs run; bulk batches: one band
+        // (packed: the launch's nb * NW strips in CTAs of 8, see window_kernel.cuh)
         const int groups = (h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps;
+        const int ctas = h->win_packed ? (nb * h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps : groups * nb;
         int nrb = 1;
-        if (groups * nb < 2 * h->nsm) nrb = std::min((2 * h->nsm + groups * nb - 1) / (groups * nb),
-                                                   std::max(1, h->cfg.height / 32));
+        if (ctas < 2 * h->nsm) nrb = std::min((2 * h->nsm + ctas - 1) / ctas, std::max(1, h->cfg.height / 32));
         wp.RB = (h->cfg.height + nrb - 1) / nrb;
         nrb = (h->cfg.height + wp.RB - 1) / wp.RB;
-        dim3 wgrid(groups, nb, nrb);
+        wp.nb = nb;
+        dim3 wgrid = h->win_packed ? dim3(ctas, 1, nrb) : dim3(groups, nb, nrb);
         prof_pair(h, 1, &pa, &pb);
         if (pa) cudaEventRecord(pa, st);
-        launch_window(h->c_win, wgrid, st, wp, h->cfg.out_format);
+        launch_window(h->c_win, wgrid, st, wp, h->cfg.out_format, h->win_packed);
         if (pb) cudaEventRecord(pb, st);
         cudaError_t e2 = cudaGetLastError();
         return e2 == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
@@ -510,7 +530,17 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
-    if (e == cudaSuccess && h->streaming) e = window_attrs(H);
+    if (h->streaming) {
+        // Packed window CTAs when more than 1/8 of the strip slots of per-window CTAs would idle
+        // (346-wide frames: 11 strips in 16 slots) and the per-warp staging fits.
+        const int groups = (h->NW + ieds::kWinWarps - 1) / ieds::kWinWarps;
+        h->win_packed = h->c_win <= 31 && 8 * (groups * ieds::kWinWarps - h->NW) > groups * ieds::kWinWarps &&
+                        ieds::window_smem_bytes(H, h->c_win, true) <= (size_t)kMaxSmem;
+        if (const char* ev = std::getenv("IEDS_WIN_PACKED"))
+            h->win_packed = std::atoi(ev) != 0 && h->c_win <= 31 &&
+                            ieds::window_smem_bytes(H, h->c_win, true) <= (size_t)kMaxSmem;
+    }
+    if (e == cudaSuccess && h->streaming) e = window_attrs(H, h->win_packed);
     if (e == cudaSuccess) e = cudaMalloc(&h->T, sizeof(uint32_t) * (size_t)h->chunk * h->NR * W);
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);

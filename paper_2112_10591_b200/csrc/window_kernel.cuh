@@ -50,14 +50,21 @@ struct WinParams {
     int RB;                             // rows per band (blockIdx.z); >= H: one band (the bulk path)
     int K_sat;                          // <= kWinLutMax
     uint32_t one;                       // 1 (runtime, so 0x10000 = one << 16 stays an IMAD operand)
+    int nb;                             // windows of this launch (the packed grid's item count)
 };
 
 // row pairs a CTA stages: H rows plus zero rows for the reads past H (steps read pairs
 // q < (H + C) / 2)
 __host__ __device__ constexpr int window_staged_pairs(int H) { return (H + 2 * kWinMaxC + 2) / 2; }
-// dynamic shared memory: [pairs][row words] uint2 {row 2q, row 2q+1}
-__host__ __device__ constexpr size_t window_smem_bytes(int H, int C) {
-    return 8ull * window_staged_pairs(H) * window_row_words(C);
+// Packed CTAs (narrow frames, C <= 31): the 8 warps take 8 consecutive (window, strip) items
+// of the launch, so no warp idles when the strips per window are not a multiple of 8; each warp
+// stages its own words w-1, w, w+1 of every row.
+constexpr int kWinPackedWords = 3;
+// dynamic shared memory: [pairs][row words] uint2 {row 2q, row 2q+1}; packed: one such array
+// of 3-word rows per warp
+__host__ __device__ constexpr size_t window_smem_bytes(int H, int C, bool packed = false) {
+    return packed ? 8ull * window_staged_pairs(H) * kWinPackedWords * kWinWarps
+                  : 8ull * window_staged_pairs(H) * window_row_words(C);
 }
 
 // squared distance x4 from row u (first of a pair) to pixel y0 + j of the window, y0 = u - C + 1
@@ -84,10 +91,10 @@ __device__ __forceinline__ void st_cs_bits(uint16_t*, uint64_t addr, uint32_t bi
     asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(addr), "h"((unsigned short)bits) : "memory");
 }
 
-template <int C, typename OutT>
+template <int C, typename OutT, int PS = window_row_words(C)>
 struct WinState {
     static constexpr bool WIDE = C > 31;                  // h needs a second word per side
-    static constexpr int RW = window_row_words(C);        // staged words per row
+    static constexpr int RW = window_row_words(C);        // staged words per row (CTA-shared staging)
     static constexpr int OFF = WIDE ? 2 : 1;              // this strip's word w is at index OFF
     using ActT = typename std::conditional<(C > 32), uint64_t, uint32_t>::type;   // a bit per step
     int H, lane;
@@ -154,7 +161,7 @@ struct WinState {
     __device__ __forceinline__ void step(const uint2* pr, ActT act, uint32_t (&P)[C]) {
         if (act & (ActT(1) << S)) {   // warp-uniform: a ballot result
             uint32_t ha, hb;
-            h_pair(pr + S * RW, ha, hb);
+            h_pair(pr + S * PS, ha, hb);   // PS: uint2 stride between staged row pairs
             const uint32_t h2a = ha * ha * 0x40004u, h2b = hb * hb * 0x40004u;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
@@ -221,17 +228,31 @@ struct WinState {
     }
 };
 
-template <int C, typename OutT>
+template <int C, typename OutT, bool PACKED = false>
 __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
+    static_assert(!PACKED || C <= 31, "packed CTAs stage one word per side");
     static_assert(C >= 2 && C <= kWinMaxC, "window size (h: <= 31 from one word, <= 63 from two)");
     static_assert(C <= 31 || C >= 34, "two-word windows start at C = 34 (the activity masks)");
-    using St = WinState<C, OutT>;
-    constexpr int kWinRowWords = St::RW;
+    constexpr int kWinRowWords = PACKED ? kWinPackedWords : window_row_words(C);   // uint2 stride between pairs
+    using St = WinState<C, OutT, kWinRowWords>;
     __shared__ uint32_t lut_s[(C <= 31 ? 1024 : kWinLutMax) + 1];   // table, raw output bit patterns
     extern __shared__ __align__(16) uint32_t wsm[];      // row pairs of E_df words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b = blockIdx.y, H = p.H, w0 = blockIdx.x * kWinWarps;
+    const int H = p.H, w0 = blockIdx.x * kWinWarps;
     const int NWP2 = p.NW + 2;
+    // this warp's strip: word w of window b (packed: item blockIdx.x * 8 + warp of the launch)
+    int b, w;
+    bool valid;
+    if constexpr (PACKED) {
+        const int item = w0 + warp;
+        valid = item < p.nb * p.NW;
+        b = valid ? item / p.NW : 0;
+        w = item - b * p.NW;
+    } else {
+        b = blockIdx.y;
+        w = w0 + warp;
+        valid = w < p.NW;
+    }
     // this CTA's band of emitted rows [ya, yb) and the row pairs u in [u_first, u_last) it
     // steps over: every row within C - 1 of the band (the first ones only warm the window up)
     const int ya = blockIdx.z * p.RB, yb = min(H, ya + p.RB);
@@ -242,7 +263,27 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     // stage words w0-1 .. w0+8 of every row (guard words / columns beyond the frame read 0)
     // plus zero rows past the end, interleaved by row pair: asynchronous 4-byte copies,
     // zero-filled where out of range, all in flight at once
-    {
+    if constexpr (PACKED) {
+        // each warp its own words w-1, w, w+1 (scratch indices w .. w+2, guards included)
+        if (valid) {
+            const uint32_t* src = p.Edf + ((size_t)b * H + u_first) * NWP2 + w;
+            constexpr int kRowsPerPass = 32 / kWinPackedWords;   // 10 rows x 3 words per pass
+            const int c = lane % kWinPackedWords, y_first = lane / kWinPackedWords;
+            const uint32_t base =
+                (uint32_t)__cvta_generic_to_shared(wsm) + 8u * (uint32_t)(warp * NPS * kWinPackedWords);
+            if (y_first < kRowsPerPass) {
+                for (int y = y_first; y < 2 * NPS; y += kRowsPerPass) {
+                    const bool ok = u_first + y < H;
+                    const uint32_t* g = ok ? src + (size_t)y * NWP2 + c : src;
+                    const uint32_t dst =
+                        base + 8u * (uint32_t)((y >> 1) * kWinPackedWords + c) + 4u * (uint32_t)(y & 1);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(g), "r"(ok ? 4 : 0)
+                                 : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    } else {
         // staged word c of a row = scratch index w0 - OFF + 1 + c (word w0 - OFF + c; guards at
         // 0 and NW + 1, anything beyond the row reads 0); staged row 0 = row u_first
         const uint32_t* src = p.Edf + ((size_t)b * H + u_first) * NWP2;
@@ -272,8 +313,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
-    const int w = w0 + warp;
-    if (w >= p.NW) return;
+    if (!valid) return;
     const int x = 32 * w + lane;
     St st;
     st.H = H;
@@ -295,7 +335,8 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
     // window must lie inside one 4 GB-aligned range (else all rotations take the checked path)
     const uint64_t last = st.op + (uint64_t)st.wb * (uint64_t)(yb - ya - 1);
     const bool fast_ok = __all_sync(0xFFFFFFFFu, (last >> 32) == (st.op >> 32));
-    const uint2* pr = pairs + warp;   // this strip's words w-OFF .. w+OFF of staged pair 0 (row u_first)
+    // this strip's words w-OFF .. w+OFF of staged pair 0 (row u_first)
+    const uint2* pr = PACKED ? pairs + warp * NPS * kWinPackedWords : pairs + warp;
     // columns within C-1 of the strip [32w - (C-1), 32w + 31 + (C-1)]: the outermost staged
     // words contribute their bits nearest the strip
     constexpr int kReach = St::WIDE ? C - 33 : C - 1;   // bits of the outermost word on each side

@@ -374,3 +374,34 @@ def test_small_batch_bands_match_bulk_batch():
             assert torch.equal(D1[0], D_all[k]), k
     ref = oracle.build_window(xy[off[0]:off[1]], c.width, c.height, wl.n_d, wl.n_f, a)
     assert np.abs(S_all[0].cpu().numpy().astype(np.float64) - ref["S"]).max() <= TOL
+
+
+@pytest.mark.parametrize("name,nwin,d_sat", [("C2", 300, None), ("C3", 20, None), ("C1", 7, 12.0), ("C2", 5, 2.5)])
+def test_packed_window_ctas_bit_identical(name, nwin, d_sat, monkeypatch):
+    """Packed window-kernel CTAs (8 strips of consecutive windows, per-warp staging; the default
+    for narrow frames such as 346 wide) against per-window CTAs (forced with IEDS_WIN_PACKED,
+    read at create): surfaces identical bit for bit, in bulk and small batches (row bands), at
+    C3 width too, and for d_sat = 12 (C = 31, the widest one-word window)."""
+    torch = _torch()
+    wl = WORKLOADS[name]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(d_sat if d_sat is not None else wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 300, nwin)
+    dev = torch.device("cuda", 0)
+    txy = torch.from_numpy(xy.view(np.int32)).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("IEDS_WIN_PACKED", mode)
+        with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0) as bld:
+            S = bld.build_batch(txy, toff)
+            one = torch.tensor([0, int(off[1] - off[0])], dtype=torch.int64, device=dev)
+            S1 = bld.build_batch(txy[:int(off[1])], one)
+            bld.sync()
+        out[mode] = (S, S1)
+    assert torch.equal(out["0"][0], out["1"][0])
+    assert torch.equal(out["0"][1], out["1"][1])
+    assert torch.equal(out["1"][1][0], out["1"][0][0])
+    k = nwin // 2
+    check_window({"S": out["1"][0].cpu().numpy()}, k, xy[off[k]:off[k + 1]], c.width, c.height, wl.n_d, wl.n_f, a,
+                 debug=False)
