@@ -221,6 +221,22 @@ struct WinState {
         if (y0 + 1 >= ya && y0 + 1 < yb) emit<false>(hi);
     }
 
+    // The remaining n pair steps from u on lie beyond the frame (u >= H: staged zero rows, no
+    // sites), so each would only shift the window and emit: step i would emit today's
+    // P[i + 1] as rows u + 2i - C + 1, +1.  Emit them in place instead -- no h, no vote, no
+    // shift.  Rows are checked against the band as in step_rolled, and emitted in the same order.
+    __device__ __forceinline__ void flush(int u, int n, const uint32_t (&P)[C]) {
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            if (i >= n) break;
+            const uint32_t v = (i + 1 < C) ? P[i + 1] : ksat4x2;
+            const uint32_t hi = __umulhi(v, k65536), lo = v - hi * 0x10000u;
+            const int y0 = u + 2 * i - (C - 1);
+            if (y0 >= ya && y0 < yb) emit<false>(lo);
+            if (y0 + 1 >= ya && y0 + 1 < yb) emit<false>(hi);
+        }
+    }
+
     // packed squared distances x4 from row u + R of a pair to pixels y0 + 2j, y0 + 2j + 1
     template <int R>
     __device__ __forceinline__ static constexpr uint32_t sq2(int j) {
@@ -379,7 +395,8 @@ __global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kern
             st.template rotation<0>(pr + q0 * kWinRowWords, act, P);
         }
     }
-    for (; u < u_last; u += 2) st.step_rolled(lp(u), u, P);
+    for (; u < u_last && u < H; u += 2) st.step_rolled(lp(u), u, P);
+    if (u < u_last) st.flush(u, (u_last - u + 1) >> 1, P);   // pairs beyond the frame
 }
 
 }  // namespace ieds
