@@ -236,9 +236,10 @@ def run_reference(args):
     return 0
 
 
-def run_config_brief(args, name, dev, stream, world, local, peak):
-    """Another §8(d) workload (e.g. C2, 346x260) on the same device: surfaces/s and the
-    whole-path HBM fraction over a few steps, inputs resident (not the metric's config)."""
+def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None):
+    """Another §8(d) workload (C2: 346x260; C5: the 1280x720 dense burst) on the same device:
+    surfaces/s and the whole-path HBM fraction over a few steps, inputs resident (not the
+    metric's config).  nwin overrides the workload's windows per GPU."""
     import torch
     import torch.distributed as dist
 
@@ -246,7 +247,7 @@ def run_config_brief(args, name, dev, stream, world, local, peak):
 
     wl = WORKLOADS[name]
     c = wl.scene
-    nwin = wl.n_windows
+    nwin = nwin or wl.n_windows
     rank = int(os.environ.get("RANK", "0"))
     xy, off = generate(name, rank * nwin, nwin)
     txy = torch.from_numpy(xy.view(np.int32)).to(dev)
@@ -278,7 +279,8 @@ def run_config_brief(args, name, dev, stream, world, local, peak):
     return {"workload": f"{name}: {c.width}x{c.height}, {nwin} windows x {c.events_per_window} events per GPU",
             "value": nwin * max(1, world) / (ms / 1e3), "unit": "surfaces/s", "ms_per_step": ms, "steps": ksteps,
             "hbm_frac_path": bytes_step / (ms / 1e3) / 1e9 / peak,
-            "note": "SURVEY §8(d) ceiling at the measured peak: 14.86 M surfaces/s"}
+            "note": "SURVEY §8(d) ceiling at the measured peak (4 B/event + 4 B/px): "
+                    f"{peak * 1e9 / (bytes_step / nwin) / 1e6:.2f} M surfaces/s"}
 
 
 def run_f4(args, dev, stream, world, local, wl):
@@ -602,6 +604,11 @@ def run_ours(args):
     if not args.no_c2 and args.config != "C2":
         c2 = run_config_brief(args, "C2", dev, stream, world, local, peak)
 
+    # the dense burst config (C5: 300k events per 1280x720 window, fill 13 %), 256 windows per GPU
+    c5 = None
+    if not args.no_c5 and args.config != "C5":
+        c5 = run_config_brief(args, "C5", dev, stream, world, local, peak, nwin=256)
+
     f4 = None
     if not args.no_f4:
         f4 = run_f4(args, dev, stream, world, local, wl)
@@ -698,6 +705,7 @@ def run_ours(args):
         "f3_fwl": f3,
         "f4_flow": f4,
         "c2_lowres": c2,
+        "c5_burst": c5,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -720,6 +728,7 @@ def main():
     ap.add_argument("--no-f3", action="store_true", help="skip the FWL (row f3) run")
     ap.add_argument("--no-f4", action="store_true", help="skip the flow consumer (row f4) run")
     ap.add_argument("--no-c2", action="store_true", help="skip the low-resolution C2 run")
+    ap.add_argument("--no-c5", action="store_true", help="skip the dense-burst C5 run")
     ap.add_argument("--f3-windows", type=int, default=128, help="C3-geometry windows of the FWL (row f3) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")
