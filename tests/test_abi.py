@@ -86,3 +86,38 @@ def test_sass_is_sm100a(lib):
         pytest.skip("cuobjdump not available")
     out = subprocess.run([exe, "--list-elf", LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_row_f_entry_points_reject_bad_arguments_without_cuda(lib):
+    """Rows f2-f4: argument and configuration errors are returned synchronously, before any CUDA
+    call (include/ieds.h), so they are checkable on a host without a GPU."""
+    from paper_2112_10591_b200._lib import IEDS_EINVAL, IedsFlowConfig
+
+    # f2 windowing and f3 FWL without a handle
+    assert lib.ieds_window_offsets(None, None, 0, 0, 1000, 1, None, None) == IEDS_EINVAL
+    assert lib.ieds_fwl_batch(None, None, None, None, None, 0, 1, None, None, 1000, None, None, None, None,
+                              None) == IEDS_EINVAL
+    # f4: every invalid flow configuration is rejected by ieds_flow_create
+    def fcfg(**kw):
+        c = IedsFlowConfig()
+        c.width, c.height, c.levels = kw.get("w", 64), kw.get("h", 48), kw.get("levels", 3)
+        for l in range(8):
+            c.iterations[l] = kw.get("it", 20)
+            c.lambda_[l] = kw.get("lam", 500.0)
+        c.gamma, c.scale, c.device = kw.get("gamma", 0.5), kw.get("scale", 255.0), -1
+        return c
+
+    h = ctypes.c_void_p()
+    bad = [dict(levels=0), dict(levels=9), dict(w=1), dict(h=1),
+           dict(w=6, h=6, levels=3),   # level 2 would be 1 x 1
+           dict(gamma=-0.1), dict(gamma=1.5), dict(scale=0.0), dict(scale=float("inf")), dict(it=-1),
+           dict(lam=-1.0), dict(lam=float("nan"))]
+    for kw in bad:
+        c = fcfg(**kw)
+        assert lib.ieds_flow_create(ctypes.byref(c), ctypes.byref(h)) == IEDS_EINVAL, kw
+        assert not h.value
+    assert lib.ieds_flow_create(None, ctypes.byref(h)) == IEDS_EINVAL
+    assert lib.ieds_flow_step(None, None, None, None, None, None) == IEDS_EINVAL
+    assert lib.ieds_flow_reset(None) == IEDS_EINVAL
+    assert lib.ieds_flow_launches_per_step(None) == 0
+    lib.ieds_flow_destroy(None)   # NULL-safe
