@@ -283,6 +283,66 @@ def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None):
                     f"{peak * 1e9 / (bytes_step / nwin) / 1e6:.2f} M surfaces/s"}
 
 
+def run_f2_windowing(args, dev, stream, world, local, wl, off, peak):
+    """Row f2: on-device Delta-T windowing (ieds_window_offsets) of the C3 stream: 1000 windows of
+    15 ms over 75 M time-ordered timestamps resident on the device.  The kernel binary-searches
+    each window start and checks the whole stream's order, so its algorithmic bytes are 8 B per
+    event (+ 8 B per offset).  The timestamps are synthetic, laid out so that the windows are
+    exactly the C3 batch's CSR windows, which the result is checked against."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_10591_b200 as ieds
+    from paper_2112_10591_b200._lib import load
+
+    dt = 15000
+    nwin = len(off) - 1
+    counts = np.diff(off)
+    k = np.repeat(np.arange(nwin, dtype=np.int64), counts)
+    j = np.arange(int(off[-1]), dtype=np.int64) - np.repeat(off[:-1], counts)
+    t = k * dt + (j * dt) // np.maximum(1, counts)[k]
+    tt = torch.from_numpy(t).to(dev)
+    del k, j, t
+    out = torch.empty(nwin + 1, dtype=torch.int64, device=dev)
+    bld = ieds.Builder(wl.scene.width, wl.scene.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
+    lib = load()
+    n = tt.numel()
+
+    def call():
+        rc = lib.ieds_window_offsets(bld._h, ctypes.c_void_p(tt.data_ptr()), n, 0, dt, nwin,
+                                     ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+        assert rc == 0, rc
+
+    for _ in range(max(1, args.warmup)):
+        call()
+    torch.cuda.synchronize(dev)
+    ok = bool(torch.equal(out.cpu(), torch.from_numpy(off)))
+    ksteps = max(1, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ksteps):
+        call()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    bld.sync()
+    bld.close()
+    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item()) / ksteps
+    gbs = (8.0 * n + 8.0 * (nwin + 1)) / (ms / 1e3) / 1e9
+    del tt, out
+    return {"metric": "Delta-T windowing of a resident event stream (ieds_window_offsets)",
+            "value": n * max(1, world) / (ms / 1e3) / 1e6, "unit": "Mev/s", "ms_per_step": ms, "steps": ksteps,
+            "windows": nwin, "events": n, "hbm_gbs": gbs, "hbm_frac": gbs / peak, "offsets_match_batch": ok,
+            "note": "algorithmic bytes 8 B/event (the order check reads every timestamp) + 8 B/offset"}
+
+
 def run_f4(args, dev, stream, world, local, wl):
     """Row f4: the stateful flow consumer (ieds_flow_step, reading R21) at the
     paper's HD settings (3 levels, weight 500, 20 sweeps) over the surfaces and
@@ -613,6 +673,11 @@ def run_ours(args):
     if not args.no_f4:
         f4 = run_f4(args, dev, stream, world, local, wl)
 
+    # row f2: on-device windowing of the resident stream
+    f2w = None
+    if not args.no_latency:
+        f2w = run_f2_windowing(args, dev, stream, world, local, wl, off, peak)
+
     # row f2: single-window latency (the paper's real-time mode): one window's
     # events -> surface, (a) events resident on the device, (b) through the host-buffer API
     lat = None
@@ -702,6 +767,7 @@ def run_ours(args):
         "f1_f16_surface": f1_f16,
         "f1_u8_normalised_log": f1_norm,
         "f2_latency": lat,
+        "f2_windowing": f2w,
         "f3_fwl": f3,
         "f4_flow": f4,
         "c2_lowres": c2,

@@ -668,7 +668,7 @@ int ieds_window_offsets(ieds_handle* h, const int64_t* t_us, int64_t n, int64_t 
     if (!g.ok) return IEDS_ECUDA;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t work = std::max<int64_t>(num_windows + 1, n);
-    const int blocks = (int)std::min<int64_t>(4 * 148, std::max<int64_t>(1, (work + 255) / 256));
+    const int blocks = (int)std::min<int64_t>(8 * h->nsm, std::max<int64_t>(1, (work + 255) / 256));
     ieds::window_offsets_kernel<<<blocks, 256, 0, st>>>(t_us, n, t0_us, dt_us, num_windows, window_offsets, h->err);
     return cudaGetLastError() == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
 }

@@ -240,3 +240,35 @@ def test_host_entry_point_variants_match_device(out):
         Sh = bld.build_batch_host(xy, off)
     assert Sh.dtype == {"u8": np.uint8, "f16": np.float16}[out]
     assert np.array_equal(Sd.cpu().numpy().view(np.uint8), Sh.view(np.uint8))
+
+
+def test_window_order_check_every_boundary():
+    """The order check of ieds_window_offsets (16-byte pair loads, the previous element from the
+    lane below): one inversion placed inside a pair, between pairs, across lane, warp-chunk
+    and grid-iteration boundaries and at the unpaired last element, on 16-byte aligned and
+    misaligned streams of odd and even length, is latched exactly when present; ordered streams
+    give the oracle's offsets."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    dt = 1000
+    with ieds.Builder(64, 48, 1, 4, device=0) as bld:
+        for n in (1, 2, 3, 257, 4096, 300001):
+            t = np.sort(rng.integers(0, 50 * dt, n)).astype(np.int64)
+            for shift in (0, 1):                       # 16-byte aligned / 8-byte aligned start
+                base = torch.zeros(n + 2, dtype=torch.int64, device=dev)
+                base[shift:shift + n] = torch.from_numpy(t).to(dev)
+                tt = base[shift:shift + n]
+                off = bld.window_offsets(tt, dt)
+                bld.sync()
+                assert np.array_equal(off.cpu().numpy(), oracle.window_offsets(t, dt)), (n, shift)
+                for i in sorted({1, 2, 63, 64, 65, 255, 256, 257, n - 1} & set(range(1, n))):
+                    bad = t.copy()
+                    bad[i] = bad[i - 1] - 1                # t[i] < t[i-1]
+                    base[shift:shift + n] = torch.from_numpy(bad).to(dev)
+                    bld.window_offsets(tt, dt)
+                    with pytest.raises(ieds.IedsOrderError):
+                        bld.sync()
