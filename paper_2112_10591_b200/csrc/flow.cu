@@ -16,14 +16,18 @@
 // halo tiles with the temporal filter in the last launch's epilogue.  One step is 3 launches from the host: the level-0 scale (reads the caller's
 // surface), one CUDA graph with every per-level kernel (captured once per pyramid parity,
 // replayed each window), and the output / masking pass (writes the caller's buffers).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/ieds.h"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -130,16 +134,20 @@ struct TbParams {
     const float2* Pt;      // with blend: the transported previous flow
     float gamma;
     int W, H;
+    int kk;                // sweeps of this launch, 1..kTbMaxK
     int blend;             // last launch of the level: write F into the level's flow state
 };
 
-template <int K>
-__global__ void __launch_bounds__(kTbThreads) jacobi_tb_kernel(TbParams q) {
-    const int W = q.W, H = q.H;
-    constexpr int TX = kTbRX - 2 * K, TY = kTbRY - 2 * K;
-    __shared__ float2 sw[2][kTbRY][kTbRX];
+// tile of a CTA: the region minus a kTbMaxK-pixel halo on every side
+constexpr int kTbTX = kTbRX - 2 * kTbMaxK, kTbTY = kTbRY - 2 * kTbMaxK;
+inline dim3 tb_grid(int W, int H) { return dim3((W + kTbTX - 1) / kTbTX, (H + kTbTY - 1) / kTbTY); }
+
+// One CTA's part of q.kk sweeps (see above): load the region of q.win, sweep, write the tile.
+__device__ __forceinline__ void tb_body(const TbParams& q, float2 (&sw)[2][kTbRY][kTbRX]) {
+    constexpr int K = kTbMaxK;
+    const int W = q.W, H = q.H, kk = q.kk;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int x0 = blockIdx.x * TX - K, y0 = blockIdx.y * TY - K;
+    const int x0 = blockIdx.x * kTbTX - K, y0 = blockIdx.y * kTbTY - K;
     float4 g[2][4];
     float2 i0[2][4];
 #pragma unroll
@@ -157,6 +165,7 @@ __global__ void __launch_bounds__(kTbThreads) jacobi_tb_kernel(TbParams q) {
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < K; ++s) {
+        if (s >= kk) break;
         const float2(*src)[kTbRX] = sw[s & 1];
         float2(*dst)[kTbRX] = sw[(s + 1) & 1];
 #pragma unroll
@@ -175,14 +184,15 @@ __global__ void __launch_bounds__(kTbThreads) jacobi_tb_kernel(TbParams q) {
             }
         __syncthreads();
     }
+    const float2(*fin)[kTbRX] = sw[kk & 1];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int rx = tx + 32 * a, ry = ty + 8 * j, gx = x0 + rx, gy = y0 + ry;
-            if (rx < K || rx >= K + TX || ry < K || ry >= K + TY || gx >= W || gy >= H) continue;
+            if (rx < K || rx >= K + kTbTX || ry < K || ry >= K + kTbTY || gx >= W || gy >= H) continue;
             const size_t p = (size_t)gy * W + gx;
-            const float2 w = sw[K & 1][ry][rx];
+            const float2 w = fin[ry][rx];
             if (q.blend) {
                 const float2 b = q.Pt[p];
                 q.wout[p] = make_float2((1.f - q.gamma) * w.x + q.gamma * b.x, (1.f - q.gamma) * w.y + q.gamma * b.y);
@@ -192,18 +202,29 @@ __global__ void __launch_bounds__(kTbThreads) jacobi_tb_kernel(TbParams q) {
         }
 }
 
-template <int K>
-void jacobi_tb(const TbParams& q, cudaStream_t st) {
-    constexpr int TX = kTbRX - 2 * K, TY = kTbRY - 2 * K;
-    jacobi_tb_kernel<K><<<dim3((q.W + TX - 1) / TX, (q.H + TY - 1) / TY), kTbThreads, 0, st>>>(q);
+__global__ void __launch_bounds__(kTbThreads) jacobi_tb_kernel(TbParams q) {
+    __shared__ float2 sw[2][kTbRY][kTbRX];
+    tb_body(q, sw);
 }
 
-void jacobi_sweeps(int k, const TbParams& q, cudaStream_t st) {
-    switch (k) {
-        case 1: jacobi_tb<1>(q, st); break;
-        case 2: jacobi_tb<2>(q, st); break;
-        case 3: jacobi_tb<3>(q, st); break;
-        default: jacobi_tb<4>(q, st); break;
+// All of a level's sweeps in one cooperative launch (levels whose tiles are all co-resident):
+// chunks of kTbMaxK sweeps with a grid-wide barrier between them, ping-ponging w0 / w1 from
+// init, the last chunk writing the filtered flow F.  Same tiles, same operations.
+__global__ void __launch_bounds__(kTbThreads) jacobi_coop_kernel(TbParams q, int sweeps, float2* w0, float2* w1,
+                                                                 float2* F) {
+    __shared__ float2 sw[2][kTbRY][kTbRX];
+    cg::grid_group grid = cg::this_grid();
+    const float2* a = q.init;
+    for (int k = 0; k < sweeps; k += kTbMaxK) {
+        const bool last = k + kTbMaxK >= sweeps;
+        TbParams c = q;
+        c.win = a;
+        c.wout = last ? F : (a == w0 ? w1 : w0);
+        c.kk = min(kTbMaxK, sweeps - k);
+        c.blend = last ? 1 : 0;
+        tb_body(c, sw);
+        if (!last) grid.sync();
+        a = c.wout;
     }
 }
 
@@ -245,6 +266,7 @@ struct ieds_flow_handle {
     bool fresh = true;
     cudaStream_t cs = nullptr;            // capture stream
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int64_t coop_blocks = 0;              // sweep CTAs that can be co-resident (0: no cooperative launch)
 };
 
 namespace {
@@ -259,6 +281,13 @@ struct FlowDevGuard {
         if (prev >= 0) cudaSetDevice(prev);
     }
 };
+
+// whether level l runs its sweeps as one cooperative launch: more than one chunk of sweeps, and
+// all of its tiles co-resident on the device
+bool coop_level(const ieds_flow_handle* h, int l) {
+    const dim3 tg = tb_grid(h->Ws[l], h->Hs[l]);
+    return h->cfg.iterations[l] > kTbMaxK && (int64_t)tg.x * tg.y <= h->coop_blocks;
+}
 
 // every per-level kernel of one non-first step, reading pyr[1-c] as previous, pyr[c] as current
 void enqueue_levels(ieds_flow_handle* h, int c, cudaStream_t st) {
@@ -284,20 +313,30 @@ void enqueue_levels(ieds_flow_handle* h, int c, cudaStream_t st) {
         }
         grad_kernel<<<pgrid(W, H), kFT, 0, st>>>(h->J1, cur + h->off[l], h->G, W, H, (float)h->cfg.lambda[l]);
         TbParams q;
+        q.win = h->init;
         q.init = h->init;
         q.G = h->G;
         q.Pt = h->Pt;
         q.gamma = (float)h->cfg.gamma;
         q.W = W;
         q.H = H;
+        const dim3 tg = tb_grid(W, H);
+        if (coop_level(h, l)) {   // every chunk in one launch, grid-wide barriers between them
+            int sweeps = K;
+            float2 *w0 = h->w0, *w1 = h->w1, *F = Pl;
+            void* args[] = {&q, &sweeps, &w0, &w1, &F};
+            cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_coop_kernel), tg, dim3(kTbThreads), args, 0, st);
+            continue;
+        }
         const float2* a = h->init;
         for (int k = 0; k < K; k += kTbMaxK) {
             const bool last = k + kTbMaxK >= K;
             float2* b = last ? Pl : (a == h->w0 ? h->w1 : h->w0);
             q.win = a;
             q.wout = b;
+            q.kk = std::min(kTbMaxK, K - k);
             q.blend = last ? 1 : 0;
-            jacobi_sweeps(std::min(kTbMaxK, K - k), q, st);
+            jacobi_tb_kernel<<<tg, kTbThreads, 0, st>>>(q);
             a = b;
         }
     }
@@ -369,6 +408,16 @@ int ieds_flow_create(const ieds_flow_config* cfg, ieds_flow_handle** out) {
     if (e == cudaSuccess) e = cudaMalloc(&h->J1, sizeof(float) * n0);
     if (e == cudaSuccess) e = cudaMalloc(&h->G, sizeof(float4) * n0);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        int coop = 0, nsm = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (coop && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, kTbThreads, 0) == cudaSuccess)
+            h->coop_blocks = (int64_t)per_sm * nsm;
+        if (const char* ev = std::getenv("IEDS_FLOW_COOP"))
+            if (std::atoi(ev) == 0) h->coop_blocks = 0;
+        cudaGetLastError();
+    }
     if (e != cudaSuccess) {
         free_flow(h);
         delete h;
@@ -442,7 +491,7 @@ int64_t ieds_flow_launches_per_step(const ieds_flow_handle* h) {
     if (!h) return 0;
     int64_t n = 2 + (h->L - 1);   // scale, down kernels, output
     for (int l = 0; l < h->L; ++l)   // prep, then grad + the sweeps (the last one blends), or a blend alone
-        n += h->cfg.iterations[l] > 0 ? 2 + (h->cfg.iterations[l] + kTbMaxK - 1) / kTbMaxK : 2;
+        n += h->cfg.iterations[l] > 0 ? 2 + (coop_level(h, l) ? 1 : (h->cfg.iterations[l] + kTbMaxK - 1) / kTbMaxK) : 2;
     return n;
 }
 

@@ -110,3 +110,28 @@ def test_flow_reset_starts_a_new_sequence():
         F, v = fe.step(torch.from_numpy(seq[0][0].astype(np.float32)).cuda())
         assert not F.any().item() and not v.any().item()
         assert fe.launches_per_step() > 0
+
+
+@pytest.mark.parametrize("iters", [(20, 20, 20), (7, 5, 13)])
+def test_flow_cooperative_sweeps_bit_identical(iters, monkeypatch):
+    """Levels whose sweep tiles are all co-resident run their sweeps as one cooperative launch
+    (grid-wide barriers between 4-sweep chunks); the same tiles and operations as one launch per
+    chunk (IEDS_FLOW_COOP=0, read at create), so the flow is identical bit for bit."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    W, H = 640, 360
+    seq = _seq(W, H, 3, 5)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("IEDS_FLOW_COOP", mode)
+        out = []
+        with ieds.FlowEstimator(W, H, iterations=iters, device=0) as fe:
+            for S, E in seq:
+                F, v = fe.step(torch.from_numpy(S.astype(np.float32)).cuda())
+                out.append(F.clone())
+            res[mode] = (out, fe.launches_per_step())
+    for a, b in zip(res["0"][0], res["1"][0]):
+        assert torch.equal(a, b)
+    assert res["1"][1] <= res["0"][1]
