@@ -398,7 +398,7 @@ def run_f4(args, dev, stream, world, local, wl):
     bld.close()
     return {"metric": "flow windows/s (3-level update-prediction flow, P:241-248, one sequence)",
             "value": 1e3 / ms, "unit": "windows/s", "ms_per_window": ms, "windows_timed": n - 4,
-            "launches_per_step": launches, "graph": "per-level kernels (prep, grad, 4 Jacobi sweeps per halo-tiled launch) replayed from one CUDA graph per step",
+            "launches_per_step": launches, "graph": "per-level kernels (prep, grad, 4 Jacobi sweeps per halo-tiled launch; the coarse levels' sweeps in one cooperative launch) replayed from one CUDA graph per step",
             "surface_plus_flow_ms_p50": float(np.median(lat[1:])),
             "note": "paper: 16.88 ms per 1280x720 window for the whole pipeline incl. its third-party flow on an "
                     "RTX 5000 (P:555); this estimator is the R21 substitute, so the timing is context, not parity"}
