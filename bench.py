@@ -7,6 +7,8 @@ batch of synthetic windows already resident in HBM: workload C3 (1280x720 Gen4-l
 windows x 75k events per GPU; N_d=2, N_f=3, d_sat=6).  Multi-GPU: one
 process per GPU (torchrun), each rank processes its own 1000 distinct windows (weak scaling,
 windows are independent: no collective in the data path); timing = max over ranks.
+--config C4 is BASELINE's sharded config instead: 16,000 windows in total split across the
+ranks (strong scaling).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
 
@@ -485,8 +487,17 @@ def run_ours(args):
     wl = WORKLOADS[args.config]
     c = wl.scene
     W, H = c.width, c.height
-    nwin = args.windows or wl.n_windows
-    k0 = shard(nwin * world, world, rank).start   # weak scaling: nwin distinct windows per rank
+    # C4 (BASELINE configs[3]) is a fixed total of windows sharded across the ranks (strong
+    # scaling); every other config gives each rank its own nwin distinct windows (weak scaling)
+    strong = args.config == "C4"
+    if strong:
+        total_windows = args.windows or wl.n_windows
+        rng = shard(total_windows, world, rank)
+        k0, nwin = rng.start, len(rng)
+    else:
+        nwin = args.windows or wl.n_windows
+        k0 = shard(nwin * world, world, rank).start
+        total_windows = nwin * world
     xy, off = generate(args.config, k0, nwin)
     n_ev = len(xy)
     txy = torch.from_numpy(xy.view(np.int32)).to(dev)
@@ -528,7 +539,6 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ms_step = ms_max / args.steps
-    total_windows = nwin * world
     value = total_windows / (ms_step / 1e3)
 
     # roofline of the dominant kernel (EDT + surface, a4-a5): algorithmic bytes = 4 B/px fp32 surface
@@ -731,7 +741,8 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u32+i32+f32", "data": "synthetic",
         "config": {"workload": f"{wl.name}: {W}x{H} Gen4-like, {nwin} windows x {c.events_per_window} events per GPU",
                    "windows_per_gpu": nwin, "events_per_gpu": n_ev, "width": W, "height": H, "n_d": wl.n_d,
