@@ -456,7 +456,7 @@ def run_f3(args, dev, stream, world, local, peak):
            "note": "algorithmic bytes 21 B/event (xy, t, p, flow gather); the I_comp/I_uncomp images are "
                    "L2 scratch (12 B/px, 16 windows per pass) that is never read back: sum I and sum I^2 come "
                    "from the atomics' old values; the bound is the L2 atomic rate, not HBM"}
-    if rank == 0 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:   # the oracle is timed at N = 1 only
         import time as _time
 
         import oracle
