@@ -325,7 +325,9 @@ void enqueue_levels(ieds_flow_handle* h, int c, cudaStream_t st) {
             int sweeps = K;
             float2 *w0 = h->w0, *w1 = h->w1, *F = Pl;
             void* args[] = {&q, &sweeps, &w0, &w1, &F};
-            cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_coop_kernel), tg, dim3(kTbThreads), args, 0, st);
+            // an error here is sticky for the capture: ieds_flow_step reports it at the end of capture
+            (void)cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_coop_kernel), tg, dim3(kTbThreads), args, 0,
+                                              st);
             continue;
         }
         const float2* a = h->init;

@@ -327,8 +327,9 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     cudaEvent_t pa, pb;
     prof_pair(h, 0, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
-    if (!stream_path && nbands > 1)   // bands OR their word rows into the column bitmap
-        cudaMemsetAsync(h->colmask, 0, sizeof(unsigned long long) * (size_t)nb * h->cfg.width, st);
+    if (!stream_path && nbands > 1 &&   // bands OR their word rows into the column bitmap
+        cudaMemsetAsync(h->colmask, 0, sizeof(unsigned long long) * (size_t)nb * h->cfg.width, st) != cudaSuccess)
+        return IEDS_ECUDA;
     // Small frames: small CTAs, several per SM, so the scatter and walk phases of different
     // windows overlap and the walk's row bands stay long (346x260, C2: the frame kernel takes
     // 0.053 / 0.038 / 0.032 / 0.030 ms per 1184 windows at 1024 / 512 / 256 / 128 threads).
@@ -399,7 +400,7 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     if (h->norm_u8) {   // row f1: q = round(255 v(D2) / v(max D2)) per window
         const int64_t npx = (int64_t)ep.W * ep.H;
         const dim3 ngrid((unsigned)std::min<int64_t>(64, (npx + ieds::kNormThreads - 1) / ieds::kNormThreads), nb);
-        cudaMemsetAsync(h->wmax, 0, sizeof(uint32_t) * nb, st);
+        if (cudaMemsetAsync(h->wmax, 0, sizeof(uint32_t) * nb, st) != cudaSuccess) return IEDS_ECUDA;
         ieds::d2max_kernel<<<ngrid, ieds::kNormThreads, 0, st>>>(D2e, npx, h->wmax);
         ieds::norm_u8_kernel<<<ngrid, ieds::kNormThreads, 0, st>>>(D2e, npx, h->wmax, h->vtab,
                                                                     static_cast<uint8_t*>(S));
@@ -746,11 +747,13 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
         fp.Iu = h->fwl_Iu;
         fp.err = h->err;
         ieds::fwl_splat_kernel<<<dim3(per_win, nb), ieds::kFwlThreads, 0, st>>>(fp, h->fwl_part);
+        cudaError_t ce = cudaSuccess;
         if (comp_image)
-            cudaMemcpy2DAsync(comp_image + (size_t)c0 * npx, sizeof(double) * npx, h->fwl_Ic, sizeof(double) * stride,
-                              sizeof(double) * npx, nb, cudaMemcpyDeviceToDevice, st);
-        cudaMemsetAsync(h->fwl_Ic, 0, sizeof(double) * stride * nb, st);   // zero for the next windows
-        cudaMemsetAsync(h->fwl_Iu, 0, sizeof(int) * stride * nb, st);
+            ce = cudaMemcpy2DAsync(comp_image + (size_t)c0 * npx, sizeof(double) * npx, h->fwl_Ic, sizeof(double) * stride,
+                                   sizeof(double) * npx, nb, cudaMemcpyDeviceToDevice, st);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(h->fwl_Ic, 0, sizeof(double) * stride * nb, st);   // zero for the next windows
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(h->fwl_Iu, 0, sizeof(int) * stride * nb, st);
+        if (ce != cudaSuccess) return IEDS_ECUDA;
         ieds::fwl_finalize_kernel<<<nb, ieds::kFwlThreads, 0, st>>>(h->fwl_part, per_win, npx, fwl + c0,
                                                                      var_comp ? var_comp + c0 : nullptr,
                                                                      var_uncomp ? var_uncomp + c0 : nullptr);
