@@ -244,8 +244,16 @@ struct WinState {
     }
 };
 
+// CTAs per SM the register budget is sized for.  Measured (ms per C3 / C2 launch; 8-bit and
+// fp16 surfaces/s at C3): C = 19 unpacked 5 / 4 / 3 CTAs: 0.827 / 0.82 / 0.828; C = 19 packed
+// (C2): 0.166 / 0.158 / 0.150; C = 8 / 10 (8-bit / fp16): 1.50 / 1.42 M at 5, 1.46 / 1.36 M at 4,
+// 1.48 / 1.40 M at 3.  (6 CTAs: 40 registers with spills, slower everywhere.)
+__host__ __device__ constexpr int window_min_ctas(int C, bool packed) {
+    return packed ? (C <= 12 ? 4 : 3) : (C <= 12 ? 5 : C <= 22 ? 4 : 3);
+}
+
 template <int C, typename OutT, bool PACKED = false>
-__global__ void __launch_bounds__(kWinWarps * 32, (C <= 22 ? 5 : 3)) window_kernel(WinParams p) {
+__global__ void __launch_bounds__(kWinWarps * 32, window_min_ctas(C, PACKED)) window_kernel(WinParams p) {
     static_assert(!PACKED || C <= 31, "packed CTAs stage one word per side");
     static_assert(C >= 2 && C <= kWinMaxC, "window size (h: <= 31 from one word, <= 63 from two)");
     static_assert(C <= 31 || C >= 34, "two-word windows start at C = 34 (the activity masks)");
