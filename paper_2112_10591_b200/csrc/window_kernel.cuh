@@ -247,9 +247,10 @@ struct WinState {
 // CTAs per SM the register budget is sized for.  Measured (ms per C3 / C2 launch; 8-bit and
 // fp16 surfaces/s at C3): C = 19 unpacked 5 / 4 / 3 CTAs: 0.827 / 0.82 / 0.828; C = 19 packed
 // (C2): 0.166 / 0.158 / 0.150; C = 8 / 10 (8-bit / fp16): 1.50 / 1.42 M at 5, 1.46 / 1.36 M at 4,
-// 1.48 / 1.40 M at 3.  (6 CTAs: 40 registers with spills, slower everywhere.)
+// 1.48 / 1.40 M at 3; C = 31 / 40 (d_sat 9 / 12): 389 / 152 k at 2, 404 / 172 k at 3, 430 /
+// 176 k at 4.  (6 CTAs: 40 registers with spills, slower everywhere.)
 __host__ __device__ constexpr int window_min_ctas(int C, bool packed) {
-    return packed ? (C <= 12 ? 4 : 3) : (C <= 12 ? 5 : C <= 22 ? 4 : 3);
+    return packed ? (C <= 12 ? 4 : 3) : (C <= 12 ? 5 : 4);
 }
 
 template <int C, typename OutT, bool PACKED = false>
