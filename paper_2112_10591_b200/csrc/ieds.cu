@@ -34,7 +34,7 @@ namespace {
 constexpr int kFrameThreads = 1024;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
 constexpr int kLutMax = ieds::kWinLutMax;
-constexpr int kSegTarget = 80;     // columns per EDT segment (warp)
+constexpr int kSegTarget = 128;   // columns per EDT segment (warp): 1280 wide = 10 segments; 48 / 64 / 80 / 112 / 128 / 144 / 160 measured 99.7 / 99.7 / 99.7 / 86.5 / 106.8 / 101.2 / 97.5 k surfaces/s at C3
 // row f3: windows per splat pass.  Each window's images are 12 B/px of scratch, hit by the
 // splat's atomics and then re-zeroed by a memset; 16 windows at 1280x720 measured best
 // (4: 118k, 8: 141k, 16: 146k, 32: 131k windows/s; 64 spills far out of L2: 63k).
