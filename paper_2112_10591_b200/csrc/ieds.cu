@@ -34,7 +34,11 @@ namespace {
 constexpr int kFrameThreads = 1024;
 constexpr int kMaxSmem = 232448;   // 227 KB opt-in per block
 constexpr int kLutMax = ieds::kWinLutMax;
-constexpr int kSegTarget = 128;   // columns per EDT segment (warp): 1280 wide = 10 segments; 48 / 64 / 80 / 112 / 128 / 144 / 160 measured 99.7 / 99.7 / 99.7 / 86.5 / 106.8 / 101.2 / 97.5 k surfaces/s at C3
+// columns per EDT segment (warp), by what the exact kernel writes.  Surfaces only (exact flag):
+// 48 / 64 / 80 / 112 / 128 / 144 / 160 measured 99.7 / 99.7 / 99.7 / 86.5 / 106.8 / 101.2 / 97.5 k
+// surfaces/s at C3 (1280 = 10 segments of 128).  With D2 written (sqdist, the normalised 8-bit
+// view): 80 gives 72.5 k, 128 62.5 k normalised surfaces/s.
+constexpr int kSegTarget = 128, kSegTargetD2 = 80;
 // row f3: windows per splat pass.  Each window's images are 12 B/px of scratch, hit by the
 // splat's atomics and then re-zeroed by a memset; 16 windows at 1280x720 measured best
 // (4: 118k, 8: 141k, 16: 146k, 32: 131k windows/s; 64 spills far out of L2: 63k).
@@ -65,6 +69,7 @@ struct ieds_handle {
     ieds_config cfg;
     int dev;
     int NW, NWP, NR, NS, SEGW;
+    int NS_d2, SEGW_d2;        // the exact kernel's segments when it writes D2
     int band_rows, nbands;     // frame kernel: rows per CTA band, bands per window (frame_kernel.cuh)
     int nsm;                   // SMs of the device (small batches spread a window over several)
     int chunk;        // windows per launch pair of the device path (scratch capacity)
@@ -378,9 +383,9 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     ep.W = h->cfg.width;
     ep.H = h->cfg.height;
     ep.NR = h->NR;
-    ep.NS = h->NS;
-    ep.SEGW = h->SEGW;
     uint32_t* D2e = (h->norm_u8 && !D2) ? h->D2n : D2;   // the normalised 8-bit view needs D2
+    ep.NS = D2e ? h->NS_d2 : h->NS;
+    ep.SEGW = D2e ? h->SEGW_d2 : h->SEGW;
     ep.S = h->norm_u8 ? nullptr : S;
     ep.D2 = D2e;
     ep.lut = h->lut;
@@ -395,7 +400,7 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     dim3 grid(h->NR, nb);
     prof_pair(h, 1, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
-    ieds::edt_kernel<<<grid, h->NS * 32, D2e ? h->smem_edt_d2 : h->smem_edt, st>>>(ep);
+    ieds::edt_kernel<<<grid, ep.NS * 32, D2e ? h->smem_edt_d2 : h->smem_edt, st>>>(ep);
     if (pb) cudaEventRecord(pb, st);
     if (h->norm_u8) {   // row f1: q = round(255 v(D2) / v(max D2)) per window
         const int64_t npx = (int64_t)ep.W * ep.H;
@@ -466,12 +471,15 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     h->NW = (W + 31) / 32;
     h->NWP = (h->NW + 1) | 1;   // odd, with >= 1 zero pad word per row
     h->NR = (H + 31) / 32;
-    int ns = (W + kSegTarget - 1) / kSegTarget;
-    ns = std::max(1, std::min(16, ns));
-    int segw = ((W + ns - 1) / ns + 7) & ~7;
-    ns = (W + segw - 1) / segw;
-    h->NS = ns;
-    h->SEGW = segw;
+    auto segments = [&](int target, int& NS, int& SEGW) {
+        int ns = (W + target - 1) / target;
+        ns = std::max(1, std::min(16, ns));
+        const int segw = ((W + ns - 1) / ns + 7) & ~7;
+        NS = (W + segw - 1) / segw;
+        SEGW = segw;
+    };
+    segments(kSegTarget, h->NS, h->SEGW);
+    segments(kSegTargetD2, h->NS_d2, h->SEGW_d2);
 
     const double alpha = cfg->alpha;
     int64_t ksat = saturation_index(*cfg);
@@ -507,10 +515,11 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     }
     h->smem_frame = frame_bytes(h->band_rows);
     h->smem_edt = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, false);
-    h->smem_edt_d2 = edt_smem_bytes(W, h->NS, h->SEGW, h->K_lut, true);
+    h->smem_edt_d2 = edt_smem_bytes(W, h->NS_d2, h->SEGW_d2, h->K_lut, true);
     // the exact EDT keeps 1-byte site offsets per segment (<= 255 columns) and its per-row data
     // in shared memory; without it the handle still serves the streaming path (no sqdist)
-    h->exact_ok = h->smem_edt_d2 <= (size_t)kMaxSmem && h->SEGW <= 255;
+    h->exact_ok = h->smem_edt_d2 <= (size_t)kMaxSmem && h->smem_edt <= (size_t)kMaxSmem && h->SEGW <= 255 &&
+                  h->SEGW_d2 <= 255;
     if (h->smem_frame > (size_t)kMaxSmem || h->NW > kFrameThreads ||   // the D&F walk: a thread per word column
         (!h->exact_ok && (!h->streaming || (cfg->flags & IEDS_FLAG_EXACT_EDT)))) {
         delete h;
@@ -530,7 +539,8 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     cudaError_t e;
     e = cudaFuncSetAttribute(ieds::frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_frame);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem_edt_d2);
+        e = cudaFuncSetAttribute(ieds::edt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max(h->smem_edt, h->smem_edt_d2));
     if (h->streaming) {
         // Packed window CTAs when more than 1/8 of the strip slots of per-window CTAs would idle
         // (346-wide frames: 11 strips in 16 slots) and the per-warp staging fits.
