@@ -32,7 +32,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from synth.events import WORKLOADS, batch_events  # noqa: E402
-from paper_2112_10591_b200.multi import shard  # noqa: E402
+
+
+def _load_multi():
+    """paper_2112_10591_b200/multi.py loaded by path: importing the package would map
+    libieds.so, and the reference arm must not load the product's native code."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "_ieds_multi", os.path.join(ROOT, "paper_2112_10591_b200", "multi.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+multi = _load_multi()
+shard = multi.shard
 
 EDT_KERNEL_NAME = "window_kernel<C> (a4 EDT, saturation-aware register window + a5 surface)"
 METRIC = "IEDS surfaces/sec and Mev/s at 1280x720 (1/2/4/8 B200), % HBM peak"
@@ -201,47 +216,126 @@ def dist_setup():
     return world, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def resolve_config(args, world: int) -> str:
+    """BASELINE.json's metric config: C3 (configs[2], 1000 windows) on one GPU; C4 (configs[3],
+    16,000 windows sharded across the ranks) when N > 1.  --config overrides."""
+    if args.config:
+        return args.config
+    return "C4" if world > 1 else "C3"
+
+
+_REF_EVENTS = []   # the reference arm's pre-generated windows (inherited by the forked workers)
+
+
+def _ref_window(i):
+    import oracle
+
+    xy, name = _REF_EVENTS[i]
+    wl = WORKLOADS[name]
+    c = wl.scene
+    oracle.build_window(xy, c.width, c.height, wl.n_d, wl.n_f, oracle.alpha_from_dsat(wl.d_sat), want=("S",))
+    return i
+
+
 def run_reference(args):
+    """This tier's reference arm: the fp64 C oracle as it stands, on the host cores.  Each step
+    is one batch of `cores` distinct windows of the same workload as our arm (one per worker
+    process); events are generated before timing, so value = windows per step / ms_per_step
+    over exactly the timed region.  Under torchrun rank 0 alone runs it."""
     world, rank, local = dist_setup()
     if rank != 0:
         return 0
     import multiprocessing as mp
 
-    wl = WORKLOADS[args.config]
+    name = resolve_config(args, world)
+    wl = WORKLOADS[name]
+    c = wl.scene
     cores = len(os.sched_getaffinity(0))
+    per_step = cores
+    nsteps = args.warmup + args.steps
+    xy, off = generate(name, 0, per_step * nsteps)   # distinct windows for every step (untimed)
+    _REF_EVENTS.clear()
+    _REF_EVENTS.extend((xy[off[b]:off[b + 1]], name) for b in range(len(off) - 1))
     pool = mp.get_context("fork").Pool(cores)
-    for _ in range(args.warmup):
-        oracle_rate(args.config, cores, cores, pool)
-    rates, walls = [], []
-    for _ in range(args.steps):
-        r, done, wall = oracle_rate(args.config, cores, cores, pool)
-        rates.append(r)
-        walls.append(wall)
+    walls = []
+    for s in range(nsteps):
+        t0 = time.perf_counter()
+        pool.map(_ref_window, range(s * per_step, (s + 1) * per_step), chunksize=1)
+        if s >= args.warmup:
+            walls.append(time.perf_counter() - t0)
     pool.close()
     pool.join()
-    value = statistics.median(rates)
-    c = wl.scene
+    ms = 1e3 * statistics.median(walls)
+    value = per_step / (ms / 1e3)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {c.width}x{c.height}, {c.events_per_window} events/window",
-                   "width": c.width, "height": c.height, "n_d": wl.n_d, "n_f": wl.n_f, "d_sat": wl.d_sat},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if name == "C4" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {c.width}x{c.height}, {c.events_per_window} events/window "
+                               f"({per_step} windows per step)",
+                   "windows_per_step": per_step, "width": c.width, "height": c.height, "n_d": wl.n_d,
+                   "n_f": wl.n_f, "d_sat": wl.d_sat},
         "mev_per_s": value * c.events_per_window / 1e6,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"each step: {cores} windows of {wl.name}, one process per core, "
-                                   "C oracle (fp64) as it stands"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu": cpu_model(), "kind": "oracle",
+                         "sample": f"each step: {per_step} distinct windows of {wl.name}, one process per core, "
+                                   "C oracle (fp64) as it stands; value = windows per step / median step wall time"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "repo_native_libs_mapped": repo_libs_mapped(),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None):
+def repo_libs_mapped() -> list[str]:
+    """Shared objects under this repo mapped into this process (the reference arm must show no
+    libieds.so: it runs the oracle only, in forked workers)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so") or ".so." in ln}
+    except OSError:
+        return []
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT))
+
+
+def cycled_batch(name, k0, nwin, pool, dev):
+    """Device CSR batch of nwin windows of `name` whose events cycle through `pool` distinct
+    generated windows k0 .. k0+pool-1 (window i carries the events of window k0 + i % pool).
+    Used where generating every window on the host would dominate the run (C5: ~120 ms per
+    window); the pool's events (>= 150 MB) exceed the 126 MB L2, so a repeat is an HBM read."""
+    import torch
+
+    pool = max(1, min(pool, nwin))
+    pxy, poff = generate(name, k0, pool)
+    lens = np.diff(poff)
+    reps, rem = divmod(nwin, pool)
+    txy_pool = torch.from_numpy(pxy.view(np.int32)).to(dev)
+    parts = [txy_pool] * reps + ([txy_pool[:int(poff[rem])]] if rem else [])
+    txy = torch.cat(parts) if len(parts) > 1 else parts[0].clone()
+    off = np.zeros(nwin + 1, np.int64)
+    off[1:] = np.cumsum(np.concatenate([np.tile(lens, reps), lens[:rem]]))
+    return txy, torch.from_numpy(off).to(dev), int(off[-1]), pool
+
+
+def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None, total=None, pool=None):
     """Another §8(d) workload (C2: 346x260; C5: the 1280x720 dense burst) on the same device:
     surfaces/s and the whole-path HBM fraction over a few steps, inputs resident (not the
-    metric's config).  nwin overrides the workload's windows per GPU."""
+    metric's config).  nwin = windows per GPU (weak scaling), or total = windows sharded across
+    the ranks (strong scaling, BASELINE's C5 shape: 16k windows on the 8 GPUs); pool = distinct
+    generated windows per rank, cycled (cycled_batch)."""
     import torch
     import torch.distributed as dist
 
@@ -249,11 +343,21 @@ def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None):
 
     wl = WORKLOADS[name]
     c = wl.scene
-    nwin = nwin or wl.n_windows
     rank = int(os.environ.get("RANK", "0"))
-    xy, off = generate(name, rank * nwin, nwin)
-    txy = torch.from_numpy(xy.view(np.int32)).to(dev)
-    toff = torch.from_numpy(off).to(dev)
+    if total:
+        rng = shard(total, world, rank)
+        k0, nwin = rng.start, len(rng)
+    else:
+        nwin = nwin or wl.n_windows
+        k0 = rank * nwin
+    if pool:
+        txy, toff, n_ev, npool = cycled_batch(name, k0, nwin, pool, dev)
+    else:
+        xy, off = generate(name, k0, nwin)
+        txy = torch.from_numpy(xy.view(np.int32)).to(dev)
+        toff = torch.from_numpy(off).to(dev)
+        n_ev, npool = int(off[-1]), nwin
+        del xy
     S = torch.empty((nwin, c.height, c.width), dtype=torch.float32, device=dev)
     bld = ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
     for _ in range(max(1, args.warmup)):
@@ -275,14 +379,19 @@ def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None):
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     ms = float(tm.item()) / ksteps
-    n_ev = int(off[-1])
     bytes_step = 4.0 * n_ev + 4.0 * c.width * c.height * nwin + 8.0 * (nwin + 1)
-    del S
-    return {"workload": f"{name}: {c.width}x{c.height}, {nwin} windows x {c.events_per_window} events per GPU",
-            "value": nwin * max(1, world) / (ms / 1e3), "unit": "surfaces/s", "ms_per_step": ms, "steps": ksteps,
+    del S, txy, toff
+    all_windows = total if total else nwin * max(1, world)
+    return {"workload": f"{name}: {c.width}x{c.height}, " + (
+                f"{total} windows sharded over {world} GPU(s) ({nwin} on rank {rank})" if total else
+                f"{nwin} windows per GPU") + f" x {c.events_per_window} events",
+            "windows_total": all_windows, "windows_per_gpu": nwin, "distinct_windows_per_gpu": npool,
+            "scaling": "strong" if total else "weak",
+            "value": all_windows / (ms / 1e3), "unit": "surfaces/s", "ms_per_step": ms, "steps": ksteps,
+            "mev_per_s": all_windows * (n_ev / nwin) / (ms / 1e3) / 1e6,
             "hbm_frac_path": bytes_step / (ms / 1e3) / 1e9 / peak,
             "note": "SURVEY §8(d) ceiling at the measured peak (4 B/event + 4 B/px): "
-                    f"{peak * 1e9 / (bytes_step / nwin) / 1e6:.2f} M surfaces/s"}
+                    f"{peak * 1e9 / (bytes_step / nwin) / 1e6:.2f} M surfaces/s per GPU"}
 
 
 def run_f2_windowing(args, dev, stream, world, local, wl, off, peak):
@@ -478,27 +587,49 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_setup()
+    dist_info = None
     if world > 1:
+        # NCCL's own communicator-init log (stderr) shows the N ranks and their transports
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()   # forces the communicator up before anything is timed
+        ws = dist.get_world_size()
+        print(f"[bench rank {rank}] process group up: backend={dist.get_backend()} world_size={ws} "
+              f"device=cuda:{local} ({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
+        if ws != world:
+            raise RuntimeError(f"WORLD_SIZE {world} but the process group has {ws} ranks")
+        try:
+            nccl_v = ".".join(str(x) for x in torch.cuda.nccl.version())
+        except Exception:
+            nccl_v = None
+        dist_info = {"backend": dist.get_backend(), "world_size": ws, "nccl_version": nccl_v,
+                     "collectives": "barrier + all_reduce(MAX) of elapsed ms + gather of sampled window digests; "
+                                    "none in the data path (windows are independent, P:113, S:198)"}
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_2112_10591_b200 as ieds
 
-    wl = WORKLOADS[args.config]
+    if args.gpus > 1 and world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    name = resolve_config(args, world)
+    wl = WORKLOADS[name]
     c = wl.scene
     W, H = c.width, c.height
     # C4 (BASELINE configs[3]) is a fixed total of windows sharded across the ranks (strong
     # scaling); every other config gives each rank its own nwin distinct windows (weak scaling)
-    strong = args.config == "C4"
+    strong = name == "C4"
     if strong:
         total_windows = args.windows or wl.n_windows
         rng = shard(total_windows, world, rank)
         k0, nwin = rng.start, len(rng)
     else:
         nwin = args.windows or wl.n_windows
-        k0 = shard(nwin * world, world, rank).start
+        rng = shard(nwin * world, world, rank)
+        k0 = rng.start
         total_windows = nwin * world
-    xy, off = generate(args.config, k0, nwin)
+    xy, off = generate(name, k0, nwin)
     n_ev = len(xy)
     txy = torch.from_numpy(xy.view(np.int32)).to(dev)
     toff = torch.from_numpy(off).to(dev)
@@ -555,11 +686,14 @@ def run_ours(args):
     path_gbs = path_bytes / (ms_step / 1e3) / 1e9
 
     # end to end through the C ABI with host buffers (copies inside the timed region)
+    # (at N > 1 on the first e2e_windows windows of each rank's shard: pinned host buffers for a
+    # whole 16k-window C4 shard would pin ~60 GB of host memory across the ranks)
     e2e = None
     if not args.no_e2e:
-        hxy = torch.from_numpy(xy.view(np.int32)).pin_memory()
-        hoff = torch.from_numpy(off).pin_memory()
-        hS = torch.empty((nwin, H, W), dtype=torch.float32).pin_memory()
+        en = min(nwin, args.e2e_windows) if world > 1 else nwin
+        hxy = torch.from_numpy(xy[:int(off[en])].view(np.int32)).pin_memory()
+        hoff = torch.from_numpy(off[:en + 1]).pin_memory()
+        hS = torch.empty((en, H, W), dtype=torch.float32).pin_memory()
         nxy, noff, nS = hxy.numpy().view(np.uint32), hoff.numpy(), hS.numpy()
         bld.build_batch_host(nxy, noff, nS)
         esteps = max(1, min(args.steps, 5))
@@ -573,12 +707,32 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = float(te.item())
-        e2e = {"value": total_windows / el, "unit": UNIT, "h2d_bytes_per_step": int(4 * n_ev + 8 * (nwin + 1)),
-               "d2h_bytes_per_step": int(4 * W * H * nwin), "steps": esteps,
-               "note": "ieds_build_batch_host: pinned host events in, pinned host surfaces out, per rank"}
+        e2e = {"value": en * world / el, "unit": UNIT, "h2d_bytes_per_step": int(4 * off[en] + 8 * (en + 1)),
+               "d2h_bytes_per_step": int(4 * W * H * en), "steps": esteps, "windows_per_rank": en,
+               "note": "ieds_build_batch_host: pinned host events in, pinned host surfaces out, per rank; "
+                       "wall clock, max over ranks"}
         del hxy, hoff, hS
 
     bld.close()
+
+    # cross-rank parity: digests of sampled windows of every rank's shard (from the timed run's
+    # surfaces), gathered to rank 0 and compared with rank 0's own recompute of those windows
+    # from regenerated events in a separate batch -- a sharded run must reproduce the
+    # single-rank results bit for bit (windows are pure functions of their events)
+    def recompute(indices):
+        out = {}
+        with ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local) as br:
+            for i in indices:
+                rxy, roff = generate(name, i, 1, procs=1)
+                rS = br.build_batch(torch.from_numpy(rxy.view(np.int32)).to(dev), torch.from_numpy(roff).to(dev))
+                br.sync()
+                out[i] = multi.window_digest(rS[0].cpu().numpy())
+        return out
+
+    mine = {i: multi.window_digest(S[i - k0].cpu().numpy()) for i in multi.sample_windows(rng, 3)}
+    xcheck = multi.cross_rank_check(mine, recompute)
+    if xcheck is not None and not xcheck["match"]:
+        print(f"cross-rank digest mismatch: {xcheck}", file=sys.stderr, flush=True)
 
     # the uncapped exact-EDT kernel on the same inputs (reported beside the headline path)
     exact = None
@@ -664,34 +818,38 @@ def run_ours(args):
                                "algorithmic bytes 4 B/event + 1 B/px", kernel_frac=False)
 
     # row f3: flow-compensated event image + FWL on C3-geometry moving scenes
+    # (rows f2-f4 are single-stream / latency measurements: N = 1 only)
+    single = world == 1
     f3 = None
-    if not args.no_f3:
+    if not args.no_f3 and single:
         f3 = run_f3(args, dev, stream, world, local, peak)
 
-    # row f4: the flow consumer (P:241-248) on consecutive C3 surfaces
-    # the low-resolution config of SURVEY §8(d) (C2: 346x260, 10,000 windows per GPU)
+    # the low-resolution config of SURVEY §8(d) (C2: 346x260, 10,000 windows per GPU; 2,000
+    # distinct generated windows per GPU, cycled: 160 MB of events)
     c2 = None
-    if not args.no_c2 and args.config != "C2":
-        c2 = run_config_brief(args, "C2", dev, stream, world, local, peak)
+    if not args.no_c2 and name != "C2":
+        c2 = run_config_brief(args, "C2", dev, stream, world, local, peak, pool=2000)
 
-    # the dense burst config (C5: 300k events per 1280x720 window, fill 13 %), 256 windows per GPU
+    # the dense burst config at BASELINE's shape (configs[4]: 300k events per 1280x720 window,
+    # fill 13 %; 16,000 windows sharded across the ranks; 256 distinct windows per GPU, cycled)
     c5 = None
-    if not args.no_c5 and args.config != "C5":
-        c5 = run_config_brief(args, "C5", dev, stream, world, local, peak, nwin=256)
+    if not args.no_c5 and name != "C5":
+        c5 = run_config_brief(args, "C5", dev, stream, world, local, peak, total=args.c5_windows, pool=256)
 
+    # row f4: the flow consumer (P:241-248) on consecutive C3 surfaces
     f4 = None
-    if not args.no_f4:
+    if not args.no_f4 and single:
         f4 = run_f4(args, dev, stream, world, local, wl)
 
     # row f2: on-device windowing of the resident stream
     f2w = None
-    if not args.no_latency:
+    if not args.no_latency and single:
         f2w = run_f2_windowing(args, dev, stream, world, local, wl, off, peak)
 
     # row f2: single-window latency (the paper's real-time mode): one window's
     # events -> surface, (a) events resident on the device, (b) through the host-buffer API
     lat = None
-    if not args.no_latency:
+    if not args.no_latency and single:
         bl = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local, chunk_windows=1)
         S1 = torch.empty((1, H, W), dtype=torch.float32, device=dev)
         hS1 = torch.empty((1, H, W), dtype=torch.float32).pin_memory().numpy()
@@ -734,8 +892,8 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
         n_s = max(cores, args.cpu_windows)
-        r, done, wall = oracle_rate(args.config, n_s, cores)
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
+        r, done, wall = oracle_rate(name, n_s, cores)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "cpu": cpu_model(), "kind": "oracle",
                "sample": f"{done} windows of {wl.name} (distinct seeds), {cores} processes, "
                          f"C oracle fp64 as it stands, {wall:.1f} s wall"}
 
@@ -744,8 +902,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u32+i32+f32", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {W}x{H} Gen4-like, {nwin} windows x {c.events_per_window} events per GPU",
-                   "windows_per_gpu": nwin, "events_per_gpu": n_ev, "width": W, "height": H, "n_d": wl.n_d,
+        "config": {"workload": (f"{wl.name}: {W}x{H} Gen4-like, {total_windows} windows sharded over {world} GPU(s), "
+                                if strong else f"{wl.name}: {W}x{H} Gen4-like, {nwin} windows per GPU, ")
+                               + f"{c.events_per_window} events per window",
+                   "windows_total": total_windows, "windows_per_gpu": nwin, "events_per_gpu": n_ev, "width": W, "height": H, "n_d": wl.n_d,
                    "n_f": wl.n_f, "d_sat": wl.d_sat, "alpha": bld.params.alpha,
                    "l2": "inputs+outputs larger than L2 (events %.0f MB, surfaces %.0f MB per step)" % (
                        4 * n_ev / 1e6, 4 * W * H * nwin / 1e6)},
@@ -760,16 +920,15 @@ def run_ours(args):
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": edt_bytes_per_launch, "avg_launch_ms": edt_avg_ms,
                      "share_of_step": edt_ms / max(1e-9, ms_max),
-                     "limiter": {"measured": "ALU pipe + issue (not DRAM)",
-                                 "evidence": "profiles/r01_ncu_full_frame_window.md: window_kernel "
-                                             "sm__pipe_alu_cycles_active ~70 %, issue ~75 %, DRAM ~45 %; "
-                                             "~24 lane-instructions per pixel (DESIGN §6)"}},
+                     "ncu_summary": args.ncu_summary},
         "kernels": {"frame_kernel": {"avg_ms": fr_avg_ms, "launches": fr_n,
                                      "achieved_gbs": fr_bytes_per_launch / (fr_avg_ms / 1e3) / 1e9 if fr_avg_ms else None,
                                      "share_of_step": fr_ms / max(1e-9, ms_max)},
                     "window_kernel": {"avg_ms": edt_avg_ms, "launches": edt_n,
                                       "share_of_step": edt_ms / max(1e-9, ms_max)}},
         "gpu_launches": int(launches_per_step * args.steps),
+        "dist": dist_info,
+        "cross_rank_check": xcheck,
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -796,8 +955,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
-    ap.add_argument("--windows", type=int, default=0, help="override windows per GPU (default: config)")
+    ap.add_argument("--config", default=None, choices=sorted(WORKLOADS),
+                    help="workload (default: C3 on one GPU, C4 = 16k windows sharded when N > 1)")
+    ap.add_argument("--windows", type=int, default=0,
+                    help="override windows per GPU (C4: total windows) (default: config)")
+    ap.add_argument("--c5-windows", type=int, default=16000,
+                    help="C5 dense-burst windows in total, sharded across the ranks (BASELINE configs[4])")
+    ap.add_argument("--e2e-windows", type=int, default=1000, help="windows per rank of the e2e run when N > 1")
+    ap.add_argument("--ncu-summary", default="profiles/r02_ncu_full_frame_window.md",
+                    help="committed ncu --set full summary of the dominant kernel (limiter evidence)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-EDT comparison run")
@@ -809,13 +975,16 @@ def main():
     ap.add_argument("--f3-windows", type=int, default=128, help="C3-geometry windows of the FWL (row f3) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")
-    ap.add_argument("--cpu-windows", type=int, default=256,
-                    help="oracle windows timed for cpu_baseline (~15 core-seconds at 1280x720)")
+    ap.add_argument("--cpu-windows", type=int, default=512,
+                    help="oracle windows timed for cpu_baseline (~15 core-seconds at 1280x720 on the GPU box)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per EDT launch (from profiles/), reported in roofline.traffic")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing protocol", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # the driver launches N > 1 under torchrun; a bare `bench.py --gpus N` re-runs itself that way
+        return multi.relaunch_under_torchrun(args.gpus, os.path.abspath(__file__), sys.argv[1:])
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -140,7 +140,9 @@ int ieds_build_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *w
  * copies events in and surfaces out chunk by chunk, overlapping the copies with the
  * kernels on internal streams, and returns when the surfaces are in host memory.
  * Page-locked host buffers give full PCIe bandwidth.  Grows internal buffers as needed
- * (this entry point may allocate).  Returns data errors directly (no ieds_sync needed). */
+ * (this entry point may allocate).  Returns data errors directly (no ieds_sync needed).
+ * It first synchronises the device, so device-pointer calls on this handle that are still
+ * queued on any stream finish before its internal streams reuse the handle's scratch. */
 int ieds_build_batch_host(ieds_handle *h, const uint32_t *events_xy,
                           const int64_t *window_offsets, int32_t num_windows, void *surfaces);
 
@@ -153,6 +155,55 @@ int ieds_build_batch_host(ieds_handle *h, const uint32_t *events_xy,
  * the events_xy input of ieds_build_batch.  Enqueued on `stream`; no host sync. */
 int ieds_window_offsets(ieds_handle *h, const int64_t *t_us, int64_t n, int64_t t0_us, int64_t dt_us,
                         int32_t num_windows, int64_t *window_offsets, void *stream);
+
+/* Row f2 -- the window count of a time-ordered DEVICE stream t_us [n] (reading R16):
+ * *t0_us = t_us[0] and *num_windows = floor((t_us[n-1] - t0) / dt_us) + 1 (0 when n = 0), the
+ * num_windows that ieds_window_offsets takes.  Reads the two end timestamps (two 8-byte copies
+ * on `stream`) and synchronises that stream.  t0_us / num_windows are HOST pointers.
+ * IEDS_EORDER if t_us[n-1] < t_us[0]; IEDS_ECAPACITY if the count exceeds INT32_MAX. */
+int ieds_window_count(ieds_handle *h, const int64_t *t_us, int64_t n, int64_t dt_us, int64_t *t0_us,
+                      int32_t *num_windows, void *stream);
+
+/* ---- Row f2: streaming ingest (Fig. 1 pipeline) -----------------------------
+ * The paper's accumulation thread fills a buffer event by event, and a second thread builds
+ * the image "when the time window has expired".  An ieds_stream does that for a live
+ * stream delivered in host chunks of any size: it windows the events by Delta T on the device
+ * (t0 = the first event of the stream, window k = floor((t - t0)/dt) == k, reading R16),
+ * carries the still-open window's events on the device from one push to the next, and
+ * returns the surface of every window as soon as an event of a later window arrives.
+ * Results are bit-identical to ieds_window_offsets + ieds_build_batch over the whole stream,
+ * wherever the stream is cut (tests/test_gpu_stream.py).
+ * Host buffers: t_us int64 [n] (non-decreasing across the whole stream), events_xy uint32 [n]
+ * (x | y << 16); they are staged through the stream's pinned buffers, so any host memory works.
+ * Surfaces are written to the HOST array `surfaces` ([max_out][H][W] of the handle's output
+ * type); page-locked memory gives full PCIe bandwidth.  Calls are synchronous (they return
+ * with the surfaces in host memory) and use the handle's scratch: do not interleave them with
+ * other calls on the same handle from another thread. */
+typedef struct ieds_stream ieds_stream;
+
+/* A stream on handle h (which it borrows: destroy the stream first) with window length dt_us. */
+int ieds_stream_create(ieds_handle *h, int64_t dt_us, ieds_stream **out);
+
+/* Number of windows a push of a chunk with first / last timestamps t_first_us / t_last_us
+ * would close (the capacity that push needs in `surfaces`; t_first_us sets t0 when it is the
+ * stream's first event). */
+int64_t ieds_stream_closing(const ieds_stream *s, int64_t t_first_us, int64_t t_last_us);
+
+/* Ingest n events.  Every window that ends before the window of t_us[n-1] is closed: its
+ * surface is written to surfaces[*num_out ...] (empty interior windows give the saturated
+ * surface).  max_out = capacity of `surfaces` in windows; IEDS_ECAPACITY (nothing consumed)
+ * if the push would close more.  IEDS_EORDER (the push is rejected, the stream unchanged) if
+ * the chunk starts before the stream's last timestamp or is not non-decreasing; IEDS_ERANGE
+ * if an event lies outside the frame (dropped, the push completes). */
+int ieds_stream_push(ieds_stream *s, const int64_t *t_us, const uint32_t *events_xy, int64_t n,
+                     void *surfaces, int32_t max_out, int32_t *num_out);
+
+/* End of stream: closes the open window (1 surface if any event was pushed since the last
+ * flush, else 0) and resets the stream, so the next push starts a new stream with its own t0. */
+int ieds_stream_flush(ieds_stream *s, void *surfaces, int32_t max_out, int32_t *num_out);
+
+/* NULL-safe. */
+void ieds_stream_destroy(ieds_stream *s);
 
 /* Row f3: flow-compensated event image and Flow Warping Loss of each window (PAPER P:293-297,
  * FWL = var(I_comp) / var(I_uncomp)).  For window b (events

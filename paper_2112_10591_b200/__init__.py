@@ -13,7 +13,7 @@ import dataclasses
 from ._lib import (IedsFlowConfig, IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, OUT_FORMATS, TRANSFERS, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
                    check, load)
 
-__all__ = ["Builder", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
+__all__ = ["Builder", "EventStream", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
            "IEDS_NO_EDGE", "LIB_PATH"]
 
 load()   # fail loudly at import if libieds.so is missing
@@ -163,6 +163,22 @@ class Builder:
                                       _ptr(sqdist), self._stream(stream)), "ieds_build_batch")
         return out
 
+    def window_count(self, t_us, dt_us: int, stream=None):
+        """Row f2 (ieds_window_count): (t0, K) of a time-ordered int64 timestamp tensor on this
+        device -- t0 = t[0], K = floor((t[-1] - t0)/dt) + 1 windows (reading R16).  Synchronous."""
+        import torch
+
+        self._check_dev(t_us, "t_us", (torch.int64,))
+        t0, K = ctypes.c_int64(), ctypes.c_int32()
+        check(load().ieds_window_count(self._h, _ptr(t_us), t_us.numel(), int(dt_us), ctypes.byref(t0),
+                                       ctypes.byref(K), self._stream(stream)), "ieds_window_count")
+        return t0.value, K.value
+
+    def stream(self, dt_us: int) -> "EventStream":
+        """Row f2 streaming ingest (ieds_stream_*): an EventStream that takes host chunks of a
+        time-ordered (t, xy) stream and returns each window's surface once it has closed."""
+        return EventStream(self, dt_us)
+
     def window_offsets(self, t_us, dt_us: int, stream=None):
         """Row f2: CSR offsets [K+1] (int64, on the device) of the Delta-T windows of a
         time-ordered int64 timestamp tensor t_us (window k = floor((t - t0)/dt) == k, t0 = t[0]).
@@ -176,8 +192,7 @@ class Builder:
             raise ValueError("dt_us must be > 0")
         if n == 0:
             return torch.zeros(1, dtype=torch.int64, device=self.device)
-        t0, t1 = (int(v) for v in t_us[[0, n - 1]].tolist())
-        K = max(0, (t1 - t0) // int(dt_us) + 1) if t1 >= t0 else 1
+        t0, K = self.window_count(t_us, dt_us, stream)
         off = torch.empty(K + 1, dtype=torch.int64, device=self.device)
         check(load().ieds_window_offsets(self._h, _ptr(t_us), n, t0, int(dt_us), K, _ptr(off),
                                          self._stream(stream)), "ieds_window_offsets")
@@ -240,6 +255,73 @@ class Builder:
         return out
 
 
+class EventStream:
+    """Row f2: a live event stream, host chunks in, surfaces out as windows close (Fig. 1).
+
+    push(t_us, xy) takes numpy int64 [n] timestamps (non-decreasing over the whole stream) and
+    uint32 [n] packed x | y << 16; it returns the surfaces [k, H, W] (host numpy, the builder's
+    output type) of the k windows that the chunk closed.  The open window's events stay on the
+    device until a later event (or flush()) closes it.  Windows follow reading R16 (t0 = the first
+    event; empty interior windows are emitted) and are bit-identical to the batched path."""
+
+    def __init__(self, builder: Builder, dt_us: int):
+        import numpy as np
+
+        self.builder = builder
+        self.dt_us = int(dt_us)
+        self._odt = {"u8": np.uint8, "f16": np.float16}.get(builder.out, np.float32)
+        self._s = ctypes.c_void_p()
+        check(load().ieds_stream_create(builder._h, self.dt_us, ctypes.byref(self._s)), "ieds_stream_create")
+
+    def closing(self, t_first_us: int, t_last_us: int) -> int:
+        """Windows a push of a chunk spanning [t_first_us, t_last_us] would close."""
+        return int(load().ieds_stream_closing(self._s, int(t_first_us), int(t_last_us)))
+
+    def _out(self, k):
+        import numpy as np
+
+        return np.empty((max(k, 0), self.builder.height, self.builder.width), self._odt)
+
+    def push(self, t_us, events_xy):
+        import numpy as np
+
+        t = np.ascontiguousarray(t_us, dtype=np.int64)
+        xy = np.ascontiguousarray(events_xy).view(np.uint32)
+        if t.shape != xy.shape or t.ndim != 1:
+            raise ValueError("t_us and events_xy must be 1-D arrays of the same length")
+        n = len(t)
+        out = self._out(self.closing(int(t[0]), int(t[-1])) if n else 0)
+        got = ctypes.c_int32()
+        check(load().ieds_stream_push(self._s, t.ctypes.data_as(ctypes.c_void_p), xy.ctypes.data_as(ctypes.c_void_p),
+                                      n, out.ctypes.data_as(ctypes.c_void_p), len(out), ctypes.byref(got)),
+              "ieds_stream_push")
+        return out[:got.value]
+
+    def flush(self):
+        out = self._out(1)
+        got = ctypes.c_int32()
+        check(load().ieds_stream_flush(self._s, out.ctypes.data_as(ctypes.c_void_p), 1, ctypes.byref(got)),
+              "ieds_stream_flush")
+        return out[:got.value]
+
+    def close(self):
+        if getattr(self, "_s", None) is not None and self._s.value:
+            load().ieds_stream_destroy(self._s)
+            self._s = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
 class FlowEstimator:
     """Row f4 (ieds_flow_*): the stateful flow consumer of the surfaces, DESIGN
     reading R21.  Defaults are the paper's HD settings (3 levels, weight 500, 20 sweeps
@@ -266,16 +348,27 @@ class FlowEstimator:
     def step(self, surface, edge_bits=None, out=None, stream=None):
         import torch
 
+        H, W = self.height, self.width
         if surface.dtype != torch.float32 or surface.device != self.device or not surface.is_contiguous():
             raise TypeError("surface must be a contiguous float32 tensor on the estimator's device")
-        if tuple(surface.shape[-2:]) != (self.height, self.width):
-            raise ValueError("surface shape")
-        if edge_bits is not None and (edge_bits.device != self.device or not edge_bits.is_contiguous()):
-            raise TypeError("edge_bits must be a contiguous tensor on the estimator's device")
-        flow = out if out is not None else torch.empty((self.height, self.width, 2), dtype=torch.float32,
-                                                       device=self.device)
-        valid = torch.empty((self.height, self.width), dtype=torch.uint8, device=self.device)
-        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        if tuple(surface.shape[-2:]) != (H, W) or surface.numel() != H * W:
+            raise ValueError(f"surface must hold one {H}x{W} frame, got shape {tuple(surface.shape)}")
+        if edge_bits is not None:
+            if edge_bits.device != self.device or not edge_bits.is_contiguous():
+                raise TypeError("edge_bits must be a contiguous tensor on the estimator's device")
+            if edge_bits.dtype not in (torch.int32, torch.uint32) or edge_bits.numel() < H * ((W + 31) // 32):
+                raise ValueError(f"edge_bits must be int32/uint32 with >= {H}*ceil({W}/32) words")
+        if out is not None:
+            if (out.dtype != torch.float32 or out.device != self.device or not out.is_contiguous()
+                    or tuple(out.shape) != (H, W, 2)):
+                raise ValueError(f"out must be a contiguous float32 [{H}, {W}, 2] tensor on {self.device}")
+            flow = out
+        else:
+            flow = torch.empty((H, W, 2), dtype=torch.float32, device=self.device)
+        valid = torch.empty((H, W), dtype=torch.uint8, device=self.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        st = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         check(load().ieds_flow_step(self._h, _ptr(surface), _ptr(edge_bits), _ptr(flow), _ptr(valid),
                                     ctypes.c_void_p(st)), "ieds_flow_step")
         return flow, valid

@@ -24,7 +24,8 @@ IEDS_NO_EDGE = 0xFFFFFFFF
 # every symbol include/ieds.h declares
 EXPORTS = (
     "ieds_create", "ieds_destroy", "ieds_build_batch", "ieds_build_batch_host", "ieds_sync",
-    "ieds_window_offsets", "ieds_fwl_batch", "ieds_flow_create", "ieds_flow_destroy", "ieds_flow_reset",
+    "ieds_window_offsets", "ieds_window_count", "ieds_stream_create", "ieds_stream_closing", "ieds_stream_push",
+    "ieds_stream_flush", "ieds_stream_destroy", "ieds_fwl_batch", "ieds_flow_create", "ieds_flow_destroy", "ieds_flow_reset",
     "ieds_flow_step", "ieds_flow_launches_per_step", "ieds_launches_per_batch", "ieds_profile_enable", "ieds_profile_read", "ieds_strerror", "ieds_alpha_from_dsat", "ieds_version",
 )
 
@@ -102,6 +103,18 @@ def load():
     lib.ieds_build_batch_host.restype = ctypes.c_int
     lib.ieds_window_offsets.argtypes = [P, P, i64, i64, i64, i32, P, P]
     lib.ieds_window_offsets.restype = ctypes.c_int
+    lib.ieds_window_count.argtypes = [P, P, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i32), P]
+    lib.ieds_window_count.restype = ctypes.c_int
+    lib.ieds_stream_create.argtypes = [P, i64, ctypes.POINTER(P)]
+    lib.ieds_stream_create.restype = ctypes.c_int
+    lib.ieds_stream_closing.argtypes = [P, i64, i64]
+    lib.ieds_stream_closing.restype = i64
+    lib.ieds_stream_push.argtypes = [P, P, P, i64, P, i32, ctypes.POINTER(i32)]
+    lib.ieds_stream_push.restype = ctypes.c_int
+    lib.ieds_stream_flush.argtypes = [P, P, i32, ctypes.POINTER(i32)]
+    lib.ieds_stream_flush.restype = ctypes.c_int
+    lib.ieds_stream_destroy.argtypes = [P]
+    lib.ieds_stream_destroy.restype = None
     lib.ieds_fwl_batch.argtypes = [P, P, P, P, P, i64, i32, P, P, i64, P, P, P, P, P]
     lib.ieds_fwl_batch.restype = ctypes.c_int
     lib.ieds_flow_create.argtypes = [P, P]

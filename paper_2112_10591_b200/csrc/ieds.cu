@@ -684,6 +684,34 @@ int ieds_window_offsets(ieds_handle* h, const int64_t* t_us, int64_t n, int64_t 
     return cudaGetLastError() == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
 }
 
+int ieds_window_count(ieds_handle* h, const int64_t* t_us, int64_t n, int64_t dt_us, int64_t* t0_us,
+                      int32_t* num_windows, void* stream) {
+    if (!h || n < 0 || dt_us <= 0 || !t0_us || !num_windows || (n > 0 && !t_us)) return IEDS_EINVAL;
+    *t0_us = 0;
+    *num_windows = 0;
+    if (n == 0) return IEDS_OK;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int64_t* ends = nullptr;   // pinned: t[0], t[n-1]
+    cudaError_t e = cudaMallocHost(&ends, 2 * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ends, t_us, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ends + 1, t_us + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFreeHost(ends);
+        return cuda_fail(e);
+    }
+    const int64_t t0 = ends[0], t1 = ends[1];
+    cudaFreeHost(ends);
+    *t0_us = t0;
+    if (t1 < t0) return IEDS_EORDER;
+    const int64_t K = (t1 - t0) / dt_us + 1;   // R16: windows up to the last event's
+    if (K > INT32_MAX) return IEDS_ECAPACITY;
+    *num_windows = (int32_t)K;
+    return IEDS_OK;
+}
+
 int ieds_sync(ieds_handle* h, void* stream) {
     if (!h) return IEDS_EINVAL;
     DeviceGuard g(h->dev);
@@ -698,8 +726,9 @@ int ieds_sync(ieds_handle* h, void* stream) {
     return IEDS_OK;
 }
 
-// row f3: splat blocks per window (one partial each) when `chunk` windows share a launch
-static int fwl_splat_blocks(int chunk) { return std::max(1, (4 * 148) / chunk); }
+// row f3: splat blocks per window (one partial each) when `chunk` windows share a launch:
+// about four CTAs per SM of this device in total
+static int fwl_splat_blocks(int chunk, int nsm) { return std::max(1, (4 * nsm) / chunk); }
 
 int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* events_t_us, const int8_t* events_p,
                    const int64_t* window_offsets, int64_t n_events, int32_t num_windows, const float* flow,
@@ -715,15 +744,19 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     const int64_t npx = (int64_t)W * H;
     const int64_t stride = (npx + 3) & ~3ll;   // 16-byte aligned window images in the scratch
     cudaError_t e = cudaSuccess;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!h->fwl_Ic) {
         h->fwl_chunk = kFwlChunkDefault;
         if (const char* env = std::getenv("IEDS_FWL_CHUNK")) h->fwl_chunk = std::max(1, std::min(64, std::atoi(env)));
         const int kFwlChunk = h->fwl_chunk;
         e = cudaMalloc(&h->fwl_Ic, sizeof(double) * stride * kFwlChunk);
         if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * stride * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * fwl_splat_blocks(kFwlChunk) * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMemset(h->fwl_Ic, 0, sizeof(double) * stride * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMemset(h->fwl_Iu, 0, sizeof(int) * stride * kFwlChunk);
+        if (e == cudaSuccess)
+            e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * fwl_splat_blocks(kFwlChunk, h->nsm) * kFwlChunk);
+        // zeroed on the caller's stream: a blocking cudaMemset runs on the legacy default
+        // stream, which a non-blocking caller stream does not wait for
+        if (e == cudaSuccess) e = cudaMemsetAsync(h->fwl_Ic, 0, sizeof(double) * stride * kFwlChunk, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(h->fwl_Iu, 0, sizeof(int) * stride * kFwlChunk, st);
         if (e != cudaSuccess) {
             cudaFree(h->fwl_Ic);
             cudaFree(h->fwl_Iu);
@@ -735,10 +768,9 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
             return cuda_fail(e);
         }
     }
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     // splat grid: enough blocks per window to fill the GPU several times over
     const int kFwlChunk = h->fwl_chunk;
-    const int per_win = fwl_splat_blocks(kFwlChunk);
+    const int per_win = fwl_splat_blocks(kFwlChunk, h->nsm);
     for (int c0 = 0; c0 < num_windows; c0 += kFwlChunk) {
         const int nb = std::min(kFwlChunk, num_windows - c0);
         ieds::FwlParams fp;
@@ -782,6 +814,9 @@ int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64
     if (window_offsets[num_windows] > window_offsets[0] && !events_xy) return IEDS_EINVAL;
     DeviceGuard g(h->dev);
     if (!g.ok) return IEDS_ECUDA;
+    // The internal streams reuse the handle's scratch (E_df / T / colmask): wait for every
+    // ieds_build_batch still queued on a caller stream (this entry point blocks anyway).
+    if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;
     HostPath& hp = h->hp;
     cudaError_t e = cudaSuccess;
     const size_t plane = (size_t)h->cfg.width * h->cfg.height;
@@ -837,6 +872,295 @@ int ieds_build_batch_host(ieds_handle* h, const uint32_t* events_xy, const int64
     if (e == cudaSuccess) e = cudaStreamSynchronize(hp.st[1]);
     if (e != cudaSuccess) return IEDS_ECUDA;
     return ieds_sync(h, hp.st[0]);
+}
+
+}  // extern "C"
+
+// ---- row f2: streaming ingest (include/ieds.h "streaming ingest") ------------------
+// Device buffers hold [open window's events (the carry)][this push's events]; the windowing
+// kernel finds the boundaries of the windows this push closes (and checks the order of the
+// whole span, carry included); the closed windows go through launch_chunk sub-batch by
+// sub-batch on two internal streams, each sub-batch's surfaces copied out while the next one
+// computes; the new open window's events are moved to the front of the other buffer.
+struct ieds_stream {
+    ieds_handle* h = nullptr;
+    int64_t dt = 0;
+    bool started = false;
+    int64_t t0 = 0, k_open = 0, last_t = 0;
+    int64_t cap = 0;             // device / pinned capacity in events
+    int cur = 0;                 // buffer holding the carry
+    int64_t n_carry = 0;
+    uint32_t* d_xy[2] = {nullptr, nullptr};
+    int64_t* d_t[2] = {nullptr, nullptr};
+    int64_t cap_off = 0;
+    int64_t* d_off = nullptr;    // [cap_off + 2]
+    int* d_err = nullptr;        // the stream's own order flag
+    uint32_t* p_xy = nullptr;    // pinned staging [cap]
+    int64_t* p_t = nullptr;
+    int64_t* p_io = nullptr;     // pinned: {err, carry start}
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t kdone[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+    void* d_S[2] = {nullptr, nullptr};   // host_chunk windows of surfaces each
+};
+
+namespace {
+
+void stream_free_buffers(ieds_stream* s) {
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(s->d_xy[i]);
+        cudaFree(s->d_t[i]);
+        s->d_xy[i] = nullptr;
+        s->d_t[i] = nullptr;
+    }
+    cudaFreeHost(s->p_xy);
+    cudaFreeHost(s->p_t);
+    s->p_xy = nullptr;
+    s->p_t = nullptr;
+    s->cap = 0;
+}
+
+// capacity for `need` device events (carry preserved) and `chunk` staged host events
+cudaError_t stream_reserve(ieds_stream* s, int64_t need) {
+    if (need <= s->cap) return cudaSuccess;
+    const int64_t cap = std::max<int64_t>(need, 2 * s->cap);
+    uint32_t* xy[2] = {nullptr, nullptr};
+    int64_t* t[2] = {nullptr, nullptr};
+    uint32_t* pxy = nullptr;
+    int64_t* pt = nullptr;
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaMalloc(&xy[i], sizeof(uint32_t) * cap);
+        if (e == cudaSuccess) e = cudaMalloc(&t[i], sizeof(int64_t) * cap);
+    }
+    if (e == cudaSuccess) e = cudaMallocHost(&pxy, sizeof(uint32_t) * cap);
+    if (e == cudaSuccess) e = cudaMallocHost(&pt, sizeof(int64_t) * cap);
+    if (e == cudaSuccess && s->n_carry > 0) {   // keep the open window
+        e = cudaMemcpyAsync(xy[0], s->d_xy[s->cur], sizeof(uint32_t) * s->n_carry, cudaMemcpyDeviceToDevice, s->st[0]);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(t[0], s->d_t[s->cur], sizeof(int64_t) * s->n_carry, cudaMemcpyDeviceToDevice, s->st[0]);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s->st[0]);
+    }
+    if (e != cudaSuccess) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(xy[i]);
+            cudaFree(t[i]);
+        }
+        cudaFreeHost(pxy);
+        cudaFreeHost(pt);
+        return e;
+    }
+    stream_free_buffers(s);
+    for (int i = 0; i < 2; ++i) {
+        s->d_xy[i] = xy[i];
+        s->d_t[i] = t[i];
+    }
+    s->p_xy = pxy;
+    s->p_t = pt;
+    s->cap = cap;
+    s->cur = 0;
+    return cudaSuccess;
+}
+
+// surfaces of windows [0, nw) of the CSR (d_xy, d_off) into host `out`, sub-batches of
+// host_chunk windows alternating between the two internal streams (kernels ordered through
+// events because the handle's scratch is shared; the copies overlap the next kernels)
+int stream_build(ieds_stream* s, const uint32_t* d_xy, const int64_t* d_off, int64_t n_ev, int64_t nw, void* out) {
+    ieds_handle* h = s->h;
+    const size_t plane = (size_t)h->cfg.width * h->cfg.height * out_elem_bytes(h);
+    const int chunk = h->host_chunk;
+    cudaError_t e = cudaSuccess;
+    int k = 0;
+    for (int64_t c0 = 0; c0 < nw; c0 += chunk, k ^= 1) {
+        const int nb = (int)std::min<int64_t>(chunk, nw - c0);
+        cudaStream_t st = s->st[k];
+        e = cudaEventSynchronize(s->done[k]);   // buffer k's previous copy finished
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, s->kdone[k ^ 1], 0);
+        if (e != cudaSuccess) return cuda_fail(e);
+        const int rc = launch_chunk(h, d_xy, d_off + c0, n_ev, nb, s->d_S[k], nullptr, nullptr, nullptr, nullptr, st);
+        if (rc != IEDS_OK) return rc;
+        e = cudaEventRecord(s->kdone[k], st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(static_cast<char*>(out) + (size_t)c0 * plane, s->d_S[k], plane * nb,
+                                cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(s->done[k], st);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    e = cudaStreamSynchronize(s->st[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->st[1]);
+    return e == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ieds_stream_create(ieds_handle* h, int64_t dt_us, ieds_stream** out) {
+    if (!out) return IEDS_EINVAL;
+    *out = nullptr;
+    if (!h || dt_us <= 0) return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    ieds_stream* s = new ieds_stream();
+    s->h = h;
+    s->dt = dt_us;
+    const size_t plane = (size_t)h->cfg.width * h->cfg.height * out_elem_bytes(h);
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaStreamCreateWithFlags(&s->st[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->kdone[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->done[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaMalloc(&s->d_S[i], plane * h->host_chunk);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(s->d_err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMallocHost(&s->p_io, 2 * sizeof(int64_t));
+    if (e != cudaSuccess) {
+        const int rc = cuda_fail(e);
+        cudaGetLastError();
+        ieds_stream_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return IEDS_OK;
+}
+
+void ieds_stream_destroy(ieds_stream* s) {
+    if (!s) return;
+    DeviceGuard g(s->h->dev);
+    for (int i = 0; i < 2; ++i) {
+        if (s->st[i]) cudaStreamSynchronize(s->st[i]);
+    }
+    stream_free_buffers(s);
+    for (int i = 0; i < 2; ++i) {
+        if (s->st[i]) cudaStreamDestroy(s->st[i]);
+        if (s->kdone[i]) cudaEventDestroy(s->kdone[i]);
+        if (s->done[i]) cudaEventDestroy(s->done[i]);
+        cudaFree(s->d_S[i]);
+    }
+    cudaFree(s->d_off);
+    cudaFree(s->d_err);
+    cudaFreeHost(s->p_io);
+    delete s;
+}
+
+int64_t ieds_stream_closing(const ieds_stream* s, int64_t t_first_us, int64_t t_last_us) {
+    if (!s) return 0;
+    const int64_t t0 = s->started ? s->t0 : t_first_us;
+    if (t_last_us < t0) return 0;
+    return std::max<int64_t>(0, (t_last_us - t0) / s->dt - (s->started ? s->k_open : 0));
+}
+
+int ieds_stream_push(ieds_stream* s, const int64_t* t_us, const uint32_t* events_xy, int64_t n, void* surfaces,
+                     int32_t max_out, int32_t* num_out) {
+    if (!s || !num_out || n < 0 || max_out < 0) return IEDS_EINVAL;
+    *num_out = 0;
+    if (n == 0) return IEDS_OK;
+    if (!t_us || !events_xy) return IEDS_EINVAL;
+    ieds_handle* h = s->h;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    // host-checkable order: the chunk continues the stream and its ends are ordered (the
+    // device kernel checks every adjacent pair below, before anything is built)
+    if ((s->started && t_us[0] < s->last_t) || t_us[n - 1] < t_us[0]) return IEDS_EORDER;
+    const int64_t t0 = s->started ? s->t0 : t_us[0];
+    const int64_t k_open = s->started ? s->k_open : 0;
+    const int64_t k_last = (t_us[n - 1] - t0) / s->dt;
+    const int64_t n_closed = k_last - k_open;
+    if (n_closed > max_out) return IEDS_ECAPACITY;
+    if (n_closed > 0 && !surfaces) return IEDS_EINVAL;
+    if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;   // scratch shared with queued calls
+    cudaError_t e = stream_reserve(s, s->n_carry + n);
+    if (e == cudaSuccess && n_closed + 2 > s->cap_off) {
+        cudaFree(s->d_off);
+        s->d_off = nullptr;
+        s->cap_off = 0;
+        const int64_t c = std::max<int64_t>(n_closed + 2, 2 * s->cap_off + 64);
+        e = cudaMalloc(&s->d_off, sizeof(int64_t) * c);
+        if (e == cudaSuccess) s->cap_off = c;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int cur = s->cur;
+    const int64_t n_tot = s->n_carry + n;
+    cudaStream_t st = s->st[0];
+    // pinned staging, then the chunk is appended after the carry
+    std::memcpy(s->p_t, t_us, sizeof(int64_t) * n);
+    std::memcpy(s->p_xy, events_xy, sizeof(uint32_t) * n);
+    e = cudaMemcpyAsync(s->d_t[cur] + s->n_carry, s->p_t, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(s->d_xy[cur] + s->n_carry, s->p_xy, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->d_err, 0, sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    // boundaries of windows k_open .. k_last over the whole span (offsets[n_closed] = the start
+    // of the still-open window k_last) + the order check of every adjacent pair
+    const int64_t work = std::max<int64_t>(n_closed + 2, n_tot);
+    const int blocks = (int)std::min<int64_t>(8 * h->nsm, std::max<int64_t>(1, (work + 255) / 256));
+    ieds::window_offsets_kernel<<<blocks, 256, 0, st>>>(s->d_t[cur], n_tot, t0 + k_open * s->dt, s->dt, n_closed + 1,
+                                                         s->d_off, s->d_err);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&s->p_io[0], s->d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&s->p_io[1], s->d_off + n_closed, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return IEDS_ECUDA;
+    if (*reinterpret_cast<int*>(&s->p_io[0]) & ieds::kErrOrder) return IEDS_EORDER;   // rejected, stream unchanged
+    const int64_t carry0 = s->p_io[1];
+    int rc = IEDS_OK;
+    if (n_closed > 0) {
+        e = cudaEventRecord(s->kdone[1], st);   // the first sub-batch waits for the offsets
+        if (e != cudaSuccess) return cuda_fail(e);
+        rc = stream_build(s, s->d_xy[cur], s->d_off, n_tot, n_closed, surfaces);
+        if (rc != IEDS_OK) return rc;
+    }
+    // the open window k_last (events [carry0, n_tot)) moves to the front of the other buffer
+    const int nxt = cur ^ 1;
+    const int64_t nc = n_tot - carry0;
+    e = cudaMemcpyAsync(s->d_xy[nxt], s->d_xy[cur] + carry0, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(s->d_t[nxt], s->d_t[cur] + carry0, sizeof(int64_t) * nc, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    s->cur = nxt;
+    s->n_carry = nc;
+    s->started = true;
+    s->t0 = t0;
+    s->k_open = k_last;
+    s->last_t = t_us[n - 1];
+    *num_out = (int32_t)n_closed;
+    return ieds_sync(h, st);   // waits for the carry move; latched IEDS_ERANGE of the built windows
+}
+
+int ieds_stream_flush(ieds_stream* s, void* surfaces, int32_t max_out, int32_t* num_out) {
+    if (!s || !num_out || max_out < 0) return IEDS_EINVAL;
+    *num_out = 0;
+    if (!s->started || s->n_carry == 0) {
+        s->started = false;
+        return IEDS_OK;
+    }
+    if (max_out < 1) return IEDS_ECAPACITY;
+    if (!surfaces) return IEDS_EINVAL;
+    ieds_handle* h = s->h;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;
+    if (s->cap_off < 2) {
+        cudaFree(s->d_off);
+        s->d_off = nullptr;
+        s->cap_off = 0;
+        if (cudaMalloc(&s->d_off, sizeof(int64_t) * 64) != cudaSuccess) return IEDS_ENOMEM;
+        s->cap_off = 64;
+    }
+    s->p_io[0] = 0;
+    s->p_io[1] = s->n_carry;
+    cudaStream_t st = s->st[0];
+    cudaError_t e = cudaMemcpyAsync(s->d_off, s->p_io, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventRecord(s->kdone[1], st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int rc = stream_build(s, s->d_xy[s->cur], s->d_off, s->n_carry, 1, surfaces);
+    if (rc != IEDS_OK) return rc;
+    s->started = false;
+    s->n_carry = 0;
+    s->k_open = 0;
+    *num_out = 1;
+    return ieds_sync(h, st);
 }
 
 }  // extern "C"

@@ -121,3 +121,19 @@ def test_row_f_entry_points_reject_bad_arguments_without_cuda(lib):
     assert lib.ieds_flow_reset(None) == IEDS_EINVAL
     assert lib.ieds_flow_launches_per_step(None) == 0
     lib.ieds_flow_destroy(None)   # NULL-safe
+
+
+def test_stream_entry_points_reject_bad_arguments_without_cuda(lib):
+    """Row f2 (streaming ingest, window count): argument errors are returned before any CUDA call."""
+    from paper_2112_10591_b200._lib import IEDS_EINVAL
+
+    s = ctypes.c_void_p()
+    assert lib.ieds_stream_create(None, 1000, ctypes.byref(s)) == IEDS_EINVAL and not s.value
+    assert lib.ieds_stream_create(None, 1000, None) == IEDS_EINVAL
+    n = ctypes.c_int32()
+    assert lib.ieds_stream_push(None, None, None, 0, None, 0, ctypes.byref(n)) == IEDS_EINVAL
+    assert lib.ieds_stream_flush(None, None, 0, ctypes.byref(n)) == IEDS_EINVAL
+    assert lib.ieds_stream_closing(None, 0, 5) == 0
+    lib.ieds_stream_destroy(None)   # NULL-safe
+    t0, k = ctypes.c_int64(), ctypes.c_int32()
+    assert lib.ieds_window_count(None, None, 0, 1000, ctypes.byref(t0), ctypes.byref(k), None) == IEDS_EINVAL

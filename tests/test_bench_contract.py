@@ -35,6 +35,26 @@ def test_reference_arm_json_line():
     assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["cores"] >= 1 and cb["sample"]
 
 
+def test_reference_arm_does_not_map_the_product_library():
+    d = json.loads(_run().stdout.strip().splitlines()[-1])
+    assert not any("libieds" in p for p in d["repo_native_libs_mapped"]), d["repo_native_libs_mapped"]
+
+
+def test_bare_gpus_2_relaunches_two_ranks():
+    """`bench.py --gpus 2` without torchrun re-runs itself as 2 ranks (torch.distributed.run on
+    127.0.0.1): one JSON line, from rank 0, reporting the real world size and the N > 1 config
+    (C4: BASELINE configs[3], 16k windows sharded)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, cwd=ROOT, timeout=600,
+                       env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    assert d["config"]["workload"].startswith("C4") and d["scaling"] == "strong"
+
+
 def test_reference_arm_other_ranks_exit_quietly():
     r = _run({"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0, r.stderr[-2000:]

@@ -148,3 +148,27 @@ def test_fwl_pileup_precision():
     t_ref = np.full(2, dt, np.int64)
     g = _check(xy, t, p, off, np.stack([F, F2]), t_ref, dt, W, H, comp_tol=float(n) * n * 2.0 ** -53)
     assert np.isfinite(g["fwl"]).all()
+
+
+def test_fwl_first_call_on_a_side_stream():
+    """the f3 scratch is zeroed on the caller's stream at the first call, so a first
+    call issued on a non-blocking torch side stream sees zeroed images (FWL equals the oracle's)."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    xy, t, p, off, flows, _fl, t_ref = flow_batch(DAVIS, 2, 0, 3)
+    dev = torch.device("cuda", 0)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    args = (T(xy.view(np.int32)), T(t), T(p), T(off), T(flows), T(t_ref))
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream(device=dev)
+    with ieds.Builder(DAVIS.width, DAVIS.height, 1, 4, device=0) as bld:
+        with torch.cuda.stream(side):
+            r = bld.fwl_batch(*args, DAVIS.dt_us)
+            bld.sync(stream=side)
+        g = r["fwl"].cpu().numpy()
+    for b in range(len(off) - 1):
+        sl = slice(off[b], off[b + 1])
+        ref = oracle.fwl(xy[sl], t[sl], p[sl], DAVIS.width, DAVIS.height, flows[b], t_ref[b], DAVIS.dt_us)["fwl"]
+        assert abs(g[b] - ref) <= 1e-9 * abs(ref)

@@ -135,3 +135,30 @@ def test_flow_cooperative_sweeps_bit_identical(iters, monkeypatch):
     for a, b in zip(res["0"][0], res["1"][0]):
         assert torch.equal(a, b)
     assert res["1"][1] <= res["0"][1]
+
+
+def test_flow_step_validates_arguments():
+    """step() rejects a wrong-shaped/typed `out`, short or mistyped edge bits and
+    accepts a torch.cuda.Stream object as the stream."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    dev = torch.device("cuda", 0)
+    W, H = 64, 48
+    S = torch.rand((H, W), dtype=torch.float32, device=dev)
+    with ieds.FlowEstimator(W, H, device=0) as fe:
+        with pytest.raises(ValueError):
+            fe.step(S, out=torch.empty((H, W), dtype=torch.float32, device=dev))
+        with pytest.raises(ValueError):
+            fe.step(S, out=torch.empty((H, W, 2), dtype=torch.float64, device=dev))
+        with pytest.raises(ValueError):
+            fe.step(S, edge_bits=torch.zeros(H * 2 - 1, dtype=torch.int32, device=dev))
+        with pytest.raises(ValueError):
+            fe.step(S, edge_bits=torch.zeros(H * 2, dtype=torch.float32, device=dev))
+        with pytest.raises(ValueError):
+            fe.step(torch.rand((2, H, W), dtype=torch.float32, device=dev))
+        side = torch.cuda.Stream(device=dev)
+        F, valid = fe.step(S, edge_bits=torch.zeros(H * 2, dtype=torch.int32, device=dev), stream=side)
+        side.synchronize()
+        assert F.shape == (H, W, 2) and int(valid.sum()) == 0

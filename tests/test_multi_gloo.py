@@ -35,6 +35,67 @@ def _surfaces(k0, n):
             .astype(np.float32) for b in range(n)]
 
 
+def _xcheck_worker(rank, world, port, q, corrupt):
+    """bench.py's cross-rank parity check: sampled digests of each rank's shard, gathered to
+    rank 0 and compared with rank 0's single-rank recompute (here: the oracle stands in for the
+    device path on tiny windows, test-only)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+
+    from paper_2112_10591_b200.multi import cross_rank_check, sample_windows
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = shard(N_WIN, world, rank)
+        S = _surfaces(rng.start, len(rng))
+        if corrupt and rank == 1:
+            S[-1] = S[-1].copy()
+            S[-1][0, 0] = np.nextafter(S[-1][0, 0], np.float32(2))
+        mine = {i: window_digest(S[i - rng.start]) for i in sample_windows(rng, 3)}
+        res = cross_rank_check(mine, lambda idx: {i: window_digest(_surfaces(i, 1)[0]) for i in idx})
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_two(target, *extra):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, 2, port, q) + extra) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        got = q.get(timeout=240)
+        res[got[0]] = got[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_cross_rank_check_two_ranks(corrupt):
+    res = _run_two(_xcheck_worker, corrupt)
+    assert res[1][0] is None
+    r0 = res[0][0]
+    # rank 0 holds windows 0..3, rank 1 windows 4..6: 3 samples each
+    assert r0["windows_checked"] == 6
+    assert r0["match"] is (not corrupt)
+    if corrupt:
+        assert r0["mismatched"] == [N_WIN - 1]
+
+
+def test_sample_windows():
+    from paper_2112_10591_b200.multi import sample_windows
+
+    assert sample_windows(range(0), 3) == []
+    assert sample_windows(range(5, 7), 3) == [5, 6]
+    assert sample_windows(range(100, 200), 3) == [100, 149, 199]
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK=str(rank))
