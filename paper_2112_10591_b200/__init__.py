@@ -192,7 +192,12 @@ class Builder:
             raise ValueError("dt_us must be > 0")
         if n == 0:
             return torch.zeros(1, dtype=torch.int64, device=self.device)
-        t0, K = self.window_count(t_us, dt_us, stream)
+        try:
+            t0, K = self.window_count(t_us, dt_us, stream)
+        except IedsOrderError:
+            # last timestamp before the first: one window; the kernel's order check latches
+            # IEDS_EORDER for sync(), as for any other inversion
+            t0, K = int(t_us[0].item()), 1
         off = torch.empty(K + 1, dtype=torch.int64, device=self.device)
         check(load().ieds_window_offsets(self._h, _ptr(t_us), n, t0, int(dt_us), K, _ptr(off),
                                          self._stream(stream)), "ieds_window_offsets")

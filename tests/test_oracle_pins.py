@@ -589,3 +589,45 @@ def test_flow_estimator_properties():
         fo = oracle.FlowOracle(384, 192, levels=L)
         rec[L] = np.mean([fo.step(S)[E].mean(0)[0] for S, E in seq][-4:]) / 8.0
     assert rec[3] >= 0.5 and rec[1] < 0.2
+
+
+def test_flow_pyramid_composition_reduces_to_single_level():
+    """the multi-level composition of the f4 oracle (reading R21), pinned against
+    its single-level run and the separately pinned upsample.  Two levels, zero sweeps at level 0
+    and gamma = 0: level 0's flow is then its initial flow, i.e. the x2 bilinear upsample of level
+    1's NEW flow, and level 1 -- the first pyramid level, with lambda[1] and iters[1] -- must be
+    exactly the one-level estimator run on the 2x2-mean-downsampled surfaces.  A wrong level
+    offset (lambda / sweeps of the wrong level), a wrong upsample source (the previous window's
+    flow P instead of the new one) or a wrong pyramid input fails this."""
+    W, H = 96, 64
+    seq = _square_sequence(W, H, 2, 4)
+    two = oracle.FlowOracle(W, H, levels=2, lambdas=(900.0, 40.0), iters=(0, 7), gamma=0.0)
+    # (the one-level run takes the level-1 image itself: 255-scaled, then 2x2-averaged, scale 1)
+    one = oracle.FlowOracle(W // 2, H // 2, levels=1, lambdas=(40.0,), iters=(7,), gamma=0.0, scale=1.0)
+    for k, (S, _) in enumerate(seq):
+        F2 = two.step(S)
+        F1 = one.step(oracle.downsample(255.0 * S))
+        if k == 0:
+            assert np.abs(F2).max() == 0.0 and np.abs(F1).max() == 0.0   # first window (S:345)
+            continue
+        assert np.abs(F1).max() > 1e-3                                      # a non-trivial coarse flow
+        np.testing.assert_array_equal(F2, oracle.upsample_flow(F1, W, H))
+    # the same with a different coarse weight must change the result (lambda[1] is used at level 1)
+    other = oracle.FlowOracle(W, H, levels=2, lambdas=(900.0, 4000.0), iters=(0, 7), gamma=0.0)
+    Fo = [other.step(S) for S, _ in seq]
+    assert np.abs(Fo[-1] - F2).max() > 1e-6
+
+
+def test_flow_prediction_term_is_the_self_transported_previous_flow():
+    """gamma = 1 leaves only the prediction at every level (F = gamma w + ... = Pt): the level-0
+    output is the previous level-0 flow transported by itself, Pt(p) = P(p - P(p)) (R21), read
+    from the estimator's packed per-level state (level 0 first)."""
+    W, H = 40, 30
+    rng = np.random.default_rng(3)
+    fo = oracle.FlowOracle(W, H, levels=2, lambdas=(500.0, 500.0), iters=(3, 3), gamma=1.0)
+    S0 = rng.random((H, W))
+    fo.step(S0)                                   # first window: state initialised
+    P0 = rng.normal(0.0, 2.0, (H, W, 2))
+    fo.P[:2 * W * H] = P0.ravel()                 # level 0's previous flow
+    F = fo.step(rng.random((H, W)))
+    np.testing.assert_array_equal(F, oracle.advect_flow(P0))
