@@ -214,9 +214,28 @@ int window_size_for(int c) {
 }
 
 
+// Sensor-width instantiations (window_kernel.cuh, WIDTH): the row stride is a compile-time
+// constant, so every store of a rotation is STG [base + immediate].  The paper's HD camera is
+// 1280 pixels wide (Prophesee Gen4); its three saturation windows: Eq. (1) fp32 (C = 19),
+// 8-bit (C = 8) and fp16 (C = 10) at d_sat = 6.  Every other width / window runs the generic kernel.
+constexpr int kSensorWidth = 1280;
+template <int C>
+constexpr bool kSensorInst = C == 8 || C == 10 || C == 19;
+
 template <int C, bool PK>
 void launch_window_pk(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int fmt) {
     const size_t smem = ieds::window_smem_bytes(std::min(wp.H, wp.RB), C, PK);
+    if constexpr (!PK && kSensorInst<C>) {
+        if (wp.W == kSensorWidth) {
+            if (fmt == IEDS_OUT_U8)
+                ieds::window_kernel<C, uint8_t, false, kSensorWidth><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+            else if (fmt == IEDS_OUT_F16)
+                ieds::window_kernel<C, uint16_t, false, kSensorWidth><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+            else
+                ieds::window_kernel<C, float, false, kSensorWidth><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
+            return;
+        }
+    }
     if (fmt == IEDS_OUT_U8) ieds::window_kernel<C, uint8_t, PK><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
     else if (fmt == IEDS_OUT_F16) ieds::window_kernel<C, uint16_t, PK><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
     else ieds::window_kernel<C, float, PK><<<grid, ieds::kWinWarps * 32, smem, st>>>(wp);
@@ -234,6 +253,17 @@ void launch_window_t(dim3 grid, cudaStream_t st, const ieds::WinParams& wp, int 
 template <int C, bool PK>
 cudaError_t window_attr_pk(int H) {
     const size_t smem = ieds::window_smem_bytes(H, C, PK);
+    if constexpr (!PK && kSensorInst<C>) {
+        cudaError_t e = cudaFuncSetAttribute(ieds::window_kernel<C, float, false, kSensorWidth>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ieds::window_kernel<C, uint8_t, false, kSensorWidth>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(ieds::window_kernel<C, uint16_t, false, kSensorWidth>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     cudaError_t e = cudaFuncSetAttribute(ieds::window_kernel<C, float, PK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)

@@ -91,7 +91,24 @@ __device__ __forceinline__ void st_cs_bits(uint16_t*, uint64_t addr, uint32_t bi
     asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(addr), "h"((unsigned short)bits) : "memory");
 }
 
-template <int C, typename OutT, int PS = window_row_words(C)>
+// the same store at a compile-time byte offset from the base address (STG [R.64 + imm]): used by
+// the width-specialised instantiations, whose row stride is a compile-time constant
+template <int OFF>
+__device__ __forceinline__ void st_cs_bits_at(float*, uint64_t addr, uint32_t bits) {
+    asm volatile("st.global.cs.b32 [%0+%2], %1;" ::"l"(addr), "r"(bits), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void st_cs_bits_at(uint8_t*, uint64_t addr, uint32_t bits) {
+    asm volatile("st.global.cs.u8 [%0+%2], %1;" ::"l"(addr), "r"(bits), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void st_cs_bits_at(uint16_t*, uint64_t addr, uint32_t bits) {
+    asm volatile("st.global.cs.u16 [%0+%2], %1;" ::"l"(addr), "h"((unsigned short)bits), "n"(OFF) : "memory");
+}
+
+// WIDTH > 0: a sensor-width instantiation (row stride WIDTH * sizeof(OutT) bytes known at
+// compile time; WIDTH % 32 == 0, so no lane of the frame's strips lies beyond the frame)
+template <int C, typename OutT, int PS = window_row_words(C), int WIDTH = 0>
 struct WinState {
     static constexpr bool WIDE = C > 31;                  // h needs a second word per side
     static constexpr int RW = window_row_words(C);        // staged words per row (CTA-shared staging)
@@ -157,6 +174,14 @@ struct WinState {
     // strip's words of pair u0/2 (the rotation's first), so the row reads use immediate
     // offsets; bit S of `act` says whether rows u, u+1 hold a site fewer than C columns from
     // the strip.  All emitted rows lie inside the frame (the caller guarantees it).
+    // sensor-width instantiations: table[idx4 / 4] stored at row ROW of the current rotation
+    // (op = the rotation's first row), an immediate offset -- no per-pixel address arithmetic
+    template <int ROW>
+    __device__ __forceinline__ void emit_row(uint32_t idx4) {
+        const uint32_t bits = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(lut) + idx4);
+        st_cs_bits_at<ROW * WIDTH * (int)sizeof(OutT)>(static_cast<OutT*>(nullptr), op, bits);
+    }
+
     template <int S>
     __device__ __forceinline__ void step(const uint2* pr, ActT act, uint32_t (&P)[C]) {
         if (act & (ActT(1) << S)) {   // warp-uniform: a ballot result
@@ -183,8 +208,14 @@ struct WinState {
         }
         const uint32_t v = P[(S + 1) % C];
         const uint32_t hi = __umulhi(v, k65536), lo = v - hi * 0x10000u;
-        emit<true>(lo);
-        emit<true>(hi);
+        if constexpr (WIDTH > 0) {
+            emit_row<2 * S>(lo);
+            emit_row<2 * S + 1>(hi);
+            if constexpr (S == C - 1) op += (uint64_t)(2 * C) * (WIDTH * sizeof(OutT));   // next rotation's rows
+        } else {
+            emit<true>(lo);
+            emit<true>(hi);
+        }
     }
 
     template <int S>
@@ -253,13 +284,14 @@ __host__ __device__ constexpr int window_min_ctas(int C, bool packed) {
     return packed ? (C <= 12 ? 4 : 3) : (C <= 12 ? 5 : 4);
 }
 
-template <int C, typename OutT, bool PACKED = false>
+template <int C, typename OutT, bool PACKED = false, int WIDTH = 0>
 __global__ void __launch_bounds__(kWinWarps * 32, window_min_ctas(C, PACKED)) window_kernel(WinParams p) {
     static_assert(!PACKED || C <= 31, "packed CTAs stage one word per side");
     static_assert(C >= 2 && C <= kWinMaxC, "window size (h: <= 31 from one word, <= 63 from two)");
     static_assert(C <= 31 || C >= 34, "two-word windows start at C = 34 (the activity masks)");
+    static_assert(WIDTH % 32 == 0 && 2 * C * WIDTH * (int)sizeof(OutT) < (1 << 23), "sensor width: whole strips, imm offsets");
     constexpr int kWinRowWords = PACKED ? kWinPackedWords : window_row_words(C);   // uint2 stride between pairs
-    using St = WinState<C, OutT, kWinRowWords>;
+    using St = WinState<C, OutT, kWinRowWords, WIDTH>;
     __shared__ uint32_t lut_s[(C <= 31 ? 1024 : kWinLutMax) + 1];   // table, raw output bit patterns
     extern __shared__ __align__(16) uint32_t wsm[];      // row pairs of E_df words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
