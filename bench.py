@@ -454,6 +454,62 @@ def run_f2_windowing(args, dev, stream, world, local, wl, off, peak):
             "note": "algorithmic bytes 8 B/event (the order check reads every timestamp) + 8 B/offset"}
 
 
+def run_f2_stream(args, dev, world, local, wl, xy, off, nwin=200, chunk_events=1_000_000):
+    """Row f2 streaming ingest (ieds_stream_push, Fig. 1 / P:117): the first nwin C3 windows as a
+    live time-ordered stream, pushed from pinned host memory in chunks of chunk_events events
+    (~13 windows; the open window carried across pushes on the device), surfaces returned into a
+    pinned host buffer as windows close.  Host in, host out, like e2e: PCIe-bound (3.7 MB of
+    surface per window)."""
+    import ctypes
+
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+    from paper_2112_10591_b200._lib import load
+
+    c = wl.scene
+    dt = 15000
+    nwin = min(nwin, len(off) - 1)
+    counts = np.diff(off[:nwin + 1])
+    n = int(off[nwin])
+    k = np.repeat(np.arange(nwin, dtype=np.int64), counts)
+    j = np.arange(n, dtype=np.int64) - np.repeat(off[:nwin], counts)
+    t_pin = torch.from_numpy(np.ascontiguousarray(k * dt + (j * dt) // np.maximum(1, counts)[k])).pin_memory()
+    ev_pin = torch.from_numpy(np.ascontiguousarray(xy[:n]).view(np.int32)).pin_memory()
+    t, ev = t_pin.numpy(), ev_pin.numpy()
+    lib = load()
+    cap = chunk_events // 10_000 + 4   # windows one push can close (C3 windows hold ~75k events)
+    hS = torch.empty((cap, c.height, c.width), dtype=torch.float32).pin_memory()
+    got = ctypes.c_int32()
+    bld = ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
+
+    def run_once():
+        done = 0
+        with bld.stream(dt) as st:
+            for a in range(0, n, chunk_events):
+                b = min(n, a + chunk_events)
+                rc = lib.ieds_stream_push(st._s, t[a:].ctypes.data_as(ctypes.c_void_p),
+                                          ev[a:].ctypes.data_as(ctypes.c_void_p), b - a,
+                                          ctypes.c_void_p(hS.data_ptr()), cap, ctypes.byref(got))
+                assert rc == 0, rc
+                done += got.value
+            rc = lib.ieds_stream_flush(st._s, ctypes.c_void_p(hS.data_ptr()), cap, ctypes.byref(got))
+            assert rc == 0, rc
+            done += got.value
+        return done
+
+    run_once()
+    t0 = time.perf_counter()
+    done = run_once()
+    el = time.perf_counter() - t0
+    bld.close()
+    return {"metric": "streaming ingest windows/s (ieds_stream_push: host (t, xy) chunks in, host surfaces out)",
+            "value": done / el, "unit": "windows/s", "windows": done, "events": n, "chunk_events": chunk_events,
+            "mev_per_s": n / el / 1e6, "ms_per_window": 1e3 * el / done,
+            "note": "wall clock; the first C3 windows as one time-ordered stream (15 ms windows), pushed in fixed-size "
+                    "chunks that cut windows at arbitrary points; surfaces into a pinned host buffer; PCIe-bound like e2e"}
+
+
 def run_f4(args, dev, stream, world, local, wl):
     """Row f4: the stateful flow consumer (ieds_flow_step, reading R21) at the
     paper's HD settings (3 levels, weight 500, 20 sweeps) over the surfaces and
@@ -557,11 +613,22 @@ def run_f3(args, dev, stream, world, local, peak):
     ms = float(tm.item()) / ksteps
     n_ev = int(off[-1])
     bytes_alg = 21.0 * n_ev + 8.0 * (nwin + 1) + 16.0 * nwin
+    ceil = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_f3_atomic_ceiling.json")) as f:
+            ceil = json.load(f)["events_per_s"]
+    except Exception:
+        pass
     out = {"metric": "FWL windows/s (flow-compensated event image + variance ratio, P:293-297)",
            "value": nwin * max(1, world) / (ms / 1e3), "unit": "windows/s", "ms_per_step": ms, "steps": ksteps,
            "windows": nwin, "mev_per_s": n_ev * max(1, world) / (ms / 1e3) / 1e6,
            "hbm_gbs": bytes_alg / (ms / 1e3) / 1e9, "hbm_frac": bytes_alg / (ms / 1e3) / 1e9 / peak,
            "fwl_mean": fwl_mean,
+           "atomic_ceiling": None if ceil is None else {
+               "events_per_s": ceil, "frac_whole_call": n_ev * max(1, world) / (ms / 1e3) / ceil,
+               "source": "profiles/r02_f3_atomic_ceiling.json (tools/atomic_ceiling.cu: the splat's 1 int32 + 4 fp64 "
+                         "atomics per event with no arithmetic); the splat kernel alone runs at ~0.97 of it, the "
+                         "whole call adds the scratch re-zeroing and the finalize"},
            "note": "algorithmic bytes 21 B/event (xy, t, p, flow gather); the I_comp/I_uncomp images are "
                    "L2 scratch (12 B/px, 16 windows per pass) that is never read back: sum I and sum I^2 come "
                    "from the atomics' old values; the bound is the L2 atomic rate, not HBM"}
@@ -841,10 +908,11 @@ def run_ours(args):
     if not args.no_f4 and single:
         f4 = run_f4(args, dev, stream, world, local, wl)
 
-    # row f2: on-device windowing of the resident stream
-    f2w = None
+    # row f2: on-device windowing of the resident stream, and the streaming ingest from the host
+    f2w = f2s = None
     if not args.no_latency and single:
         f2w = run_f2_windowing(args, dev, stream, world, local, wl, off, peak)
+        f2s = run_f2_stream(args, dev, world, local, wl, xy, off)
 
     # row f2: single-window latency (the paper's real-time mode): one window's
     # events -> surface, (a) events resident on the device, (b) through the host-buffer API
@@ -938,6 +1006,7 @@ def run_ours(args):
         "f1_u8_normalised_log": f1_norm,
         "f2_latency": lat,
         "f2_windowing": f2w,
+        "f2_stream": f2s,
         "f3_fwl": f3,
         "f4_flow": f4,
         "c2_lowres": c2,

@@ -174,7 +174,8 @@ int ieds_window_count(ieds_handle *h, const int64_t *t_us, int64_t n, int64_t dt
  * Results are bit-identical to ieds_window_offsets + ieds_build_batch over the whole stream,
  * wherever the stream is cut (tests/test_gpu_stream.py).
  * Host buffers: t_us int64 [n] (non-decreasing across the whole stream), events_xy uint32 [n]
- * (x | y << 16); they are staged through the stream's pinned buffers, so any host memory works.
+ * (x | y << 16); page-locked chunks are copied to the device directly, any other host memory is
+ * staged through the stream's pinned buffers (a host copy per push).
  * Surfaces are written to the HOST array `surfaces` ([max_out][H][W] of the handle's output
  * type); page-locked memory gives full PCIe bandwidth.  Calls are synchronous (they return
  * with the surfaces in host memory) and use the handle's scratch: do not interleave them with

@@ -288,8 +288,14 @@ class EventStream:
         return np.empty((max(k, 0), self.builder.height, self.builder.width), self._odt)
 
     def push(self, t_us, events_xy):
+        """t_us / events_xy: numpy arrays, or CPU torch tensors (pinned ones skip the library's
+        host staging copy)."""
         import numpy as np
 
+        if hasattr(t_us, "numpy"):      # CPU torch tensors: same memory, no copy
+            t_us = t_us.numpy()
+        if hasattr(events_xy, "numpy"):
+            events_xy = events_xy.numpy()
         t = np.ascontiguousarray(t_us, dtype=np.int64)
         xy = np.ascontiguousarray(events_xy).view(np.uint32)
         if t.shape != xy.shape or t.ndim != 1:

@@ -107,7 +107,8 @@ __device__ __forceinline__ void st_cs_bits_at(uint16_t*, uint64_t addr, uint32_t
 }
 
 // WIDTH > 0: a sensor-width instantiation (row stride WIDTH * sizeof(OutT) bytes known at
-// compile time; WIDTH % 32 == 0, so no lane of the frame's strips lies beyond the frame)
+// compile time).  When WIDTH % 32 != 0 the lanes of the last strip beyond the frame skip the
+// rotations' stores (a loop-invariant predicate) and keep the ragged-strip sink for the rest.
 template <int C, typename OutT, int PS = window_row_words(C), int WIDTH = 0>
 struct WinState {
     static constexpr bool WIDE = C > 31;                  // h needs a second word per side
@@ -122,6 +123,7 @@ struct WinState {
     uint32_t one;                      // 1 (runtime: the split updates' adds stay IMADs)
     uint32_t ksat4x2;                  // 4*K_sat in both halves: the start value of every slot
     const uint32_t* lut;               // shared table, raw output bit patterns
+    bool xok;                          // this lane's column lies inside the frame
 
     // h of a row for this lane from its strip's words (w-1, w, w+1), clamped to <= 31:
     // clz of (columns x-31..x with x at the MSB) | bitreverse(columns x..x+31) -- the leading
@@ -179,7 +181,7 @@ struct WinState {
     template <int ROW>
     __device__ __forceinline__ void emit_row(uint32_t idx4) {
         const uint32_t bits = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(lut) + idx4);
-        st_cs_bits_at<ROW * WIDTH * (int)sizeof(OutT)>(static_cast<OutT*>(nullptr), op, bits);
+        if (WIDTH % 32 == 0 || xok) st_cs_bits_at<ROW * WIDTH * (int)sizeof(OutT)>(static_cast<OutT*>(nullptr), op, bits);
     }
 
     template <int S>
@@ -211,7 +213,7 @@ struct WinState {
         if constexpr (WIDTH > 0) {
             emit_row<2 * S>(lo);
             emit_row<2 * S + 1>(hi);
-            if constexpr (S == C - 1) op += (uint64_t)(2 * C) * (WIDTH * sizeof(OutT));   // next rotation's rows
+            if constexpr (S == C - 1) op += (uint64_t)(2 * C) * wb;   // next rotation's rows (sink lanes: wb = 0)
         } else {
             emit<true>(lo);
             emit<true>(hi);
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, window_min_ctas(C, PACKED)) wi
     static_assert(!PACKED || C <= 31, "packed CTAs stage one word per side");
     static_assert(C >= 2 && C <= kWinMaxC, "window size (h: <= 31 from one word, <= 63 from two)");
     static_assert(C <= 31 || C >= 34, "two-word windows start at C = 34 (the activity masks)");
-    static_assert(WIDTH % 32 == 0 && 2 * C * WIDTH * (int)sizeof(OutT) < (1 << 23), "sensor width: whole strips, imm offsets");
+    static_assert(2 * C * WIDTH * (int)sizeof(OutT) < (1 << 23), "sensor width: immediate store offsets");
     constexpr int kWinRowWords = PACKED ? kWinPackedWords : window_row_words(C);   // uint2 stride between pairs
     using St = WinState<C, OutT, kWinRowWords, WIDTH>;
     __shared__ uint32_t lut_s[(C <= 31 ? 1024 : kWinLutMax) + 1];   // table, raw output bit patterns
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kWinWarps * 32, window_min_ctas(C, PACKED)) wi
     st.one = p.one;
     st.ksat4x2 = (4u * (uint32_t)p.K_sat) * 0x10001u;
     st.lut = lut_s;
+    st.xok = x < p.W;
     if (x < p.W) {
         st.op = reinterpret_cast<uint64_t>(reinterpret_cast<OutT*>(p.S) + (((size_t)b * H + ya) * p.W + x));
         st.wb = (uint32_t)(p.W * sizeof(OutT));
