@@ -43,7 +43,20 @@ struct FrameParams {
     uint32_t* __restrict__ Edf_scratch;     // [nb][H][NW+2] E_df for the streaming surface kernel,
                                             // word w at 1 + w, zero guard words at 0 and NW + 1
     int* __restrict__ err;
+    int nb;                                 // windows of this launch
+    int prefetch_ahead;                     // > 0: L2-prefetch the events of window b + this (one wave later)
+    int64_t prefetch_max;                   // bytes prefetched per window at most (a wave's share of L2)
 };
+
+// bulk prefetch of [p, p + bytes) into L2 (cp.async.bulk.prefetch; 16-byte granules, one thread)
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+    const uintptr_t a0 = (reinterpret_cast<uintptr_t>(p) + 15) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + (uintptr_t)bytes) & ~(uintptr_t)15;
+    for (uintptr_t a = a0; a < a1; a += 65536) {
+        const uint32_t n = (uint32_t)min((uintptr_t)65536, a1 - a);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    }
+}
 
 // bit-sliced "at least n of the four neighbour words are set", per bit position
 __device__ __forceinline__ uint32_t at_least(int n, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -292,6 +305,12 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(FrameParams p) {
                                        : scatter_window<true>(fr1, p, o0, o1, ya, yb, tid, nthr);
     if (bad) atomicOr(p.err, kErrRange);
     __syncthreads();
+    // the window one wave later starts when this wave's CTAs finish: stage its events in L2 now,
+    // while this CTA's walk keeps the SM busy without HBM reads
+    if (p.prefetch_ahead > 0 && tid == 0 && blockIdx.y == 0 && b + p.prefetch_ahead < p.nb) {
+        const int64_t q0 = p.offsets[b + p.prefetch_ahead], q1 = p.offsets[b + p.prefetch_ahead + 1];
+        if (q0 >= 0 && q1 > q0 && q1 <= p.n_events) prefetch_l2(p.xy + q0, min(4 * (q1 - q0), p.prefetch_max));
+    }
 
     if (p.E_out) {
         uint32_t* out = p.E_out + (size_t)b * p.H * p.NW;

@@ -72,6 +72,7 @@ struct ieds_handle {
     int NS_d2, SEGW_d2;        // the exact kernel's segments when it writes D2
     int band_rows, nbands;     // frame kernel: rows per CTA band, bands per window (frame_kernel.cuh)
     int nsm;                   // SMs of the device (small batches spread a window over several)
+    int l2_bytes;              // L2 size of the device
     int chunk;        // windows per launch pair of the device path (scratch capacity)
     int host_chunk;   // windows per pipelined copy/compute step of the host path (<= chunk)
     size_t smem_frame, smem_edt, smem_edt_d2;
@@ -352,6 +353,14 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     fp.n_d = h->cfg.n_d;
     fp.n_f = h->cfg.n_f;
     fp.vec_ok = ((reinterpret_cast<uintptr_t>(xy) & 15u) == 0) ? 1 : 0;
+    fp.nb = nb;
+    // one CTA per SM (large frames): the CTA of window b + nsm starts about a window later.  A
+    // wave's prefetches are capped at half the L2 (the first l2 / (2 nsm) bytes of each window):
+    // C3 windows (300 KB) are staged whole, C5's 1.2 MB ones partly -- whole ones thrashed the L2
+    // (C5 649 k -> 630 k surfaces/s) while C3 gained (frame kernel 0.146 -> 0.134 ms).
+    fp.prefetch_ahead = (nbands == 1 && smem_frame > (size_t)kMaxSmem / 2) ? h->nsm : 0;
+    fp.prefetch_max = (int64_t)h->l2_bytes / (2 * h->nsm) & ~15ll;
+    if (const char* ev = std::getenv("IEDS_FRAME_PREFETCH")) fp.prefetch_ahead = std::atoi(ev) ? fp.prefetch_ahead : 0;
     fp.T = h->T;
     fp.colmask = h->colmask;
     fp.E_out = E;
@@ -565,6 +574,9 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     h->nsm = nsm;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    h->l2_bytes = l2 > 0 ? l2 : (64 << 20);
     // Default: 8 waves of windows per launch pair (~143 MB of scratch at 1280x720), so a
     // 1000-window batch is one frame launch + one window launch with a single partial tail
     // wave instead of four launch pairs whose last one runs a mostly idle wave.  The host
