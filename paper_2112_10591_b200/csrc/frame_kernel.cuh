@@ -238,8 +238,12 @@ __device__ __forceinline__ void streaming_denoise_fill(const uint32_t* fr1, cons
     }
 }
 
-// a1 for one window (and band): every event of [o0, o1), 16-byte streaming loads with 4 in
-// flight per thread; returns nonzero if any event lies outside the frame
+// a1 for one window (and band): every event of [o0, o1), 16-byte streaming loads with
+// kScatterLoads in flight per thread; returns nonzero if any event lies outside the frame
+#ifndef IEDS_SCATTER_LOADS
+#define IEDS_SCATTER_LOADS 4
+#endif
+constexpr int kScatterLoads = IEDS_SCATTER_LOADS;
 template <bool BANDED>
 __device__ __forceinline__ uint32_t scatter_window(uint32_t* fr1, const FrameParams& p, int64_t o0, int64_t o1, int ya,
                                                    int yb, int tid, int nthr) {
@@ -253,13 +257,16 @@ __device__ __forceinline__ uint32_t scatter_window(uint32_t* fr1, const FramePar
         const uint4* x4 = reinterpret_cast<const uint4*>(p.xy);
         int64_t j = (h1 >> 2) + tid;
         const int64_t j1 = v1 >> 2;
-        for (; j + 3 * nthr < j1; j += 4 * nthr) {   // 4 loads in flight per thread
-            uint4 q0 = ld_stream_u4(x4 + j), q1 = ld_stream_u4(x4 + j + nthr);
-            uint4 q2 = ld_stream_u4(x4 + j + 2 * nthr), q3 = ld_stream_u4(x4 + j + 3 * nthr);
-            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q0.w);
-            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q1.w);
-            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q2.w);
-            bad |= scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.y) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q3.w);
+        auto apply4 = [&](const uint4& q) {
+            return scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.x) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.y) |
+                   scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.z) | scatter_event<BANDED>(fr1, lim, NWP, ya, yb, q.w);
+        };
+        for (; j + (kScatterLoads - 1) * nthr < j1; j += kScatterLoads * nthr) {   // kScatterLoads loads in flight
+            uint4 q[kScatterLoads];
+#pragma unroll
+            for (int r = 0; r < kScatterLoads; ++r) q[r] = ld_stream_u4(x4 + j + r * nthr);
+#pragma unroll
+            for (int r = 0; r < kScatterLoads; ++r) bad |= apply4(q[r]);
         }
         for (; j < j1; j += nthr) {
             uint4 q = ld_stream_u4(x4 + j);
