@@ -655,12 +655,20 @@ def run_ours(args):
 
     world, rank, local = dist_setup()
     dist_info = None
+    # IEDS_BENCH_SHARE_GPU=1 (code-path check only, never a measurement): every rank on cuda:0
+    # with the gloo backend, so the N > 1 path can be exercised on a one-GPU box
+    share = os.environ.get("IEDS_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
         # NCCL's own communicator-init log (stderr) shows the N ranks and their transports
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()   # forces the communicator up before anything is timed
         ws = dist.get_world_size()
         print(f"[bench rank {rank}] process group up: backend={dist.get_backend()} world_size={ws} "
@@ -672,6 +680,7 @@ def run_ours(args):
         except Exception:
             nccl_v = None
         dist_info = {"backend": dist.get_backend(), "world_size": ws, "nccl_version": nccl_v,
+                     "shared_gpu_code_path_check": share,
                      "collectives": "barrier + all_reduce(MAX) of elapsed ms + gather of sampled window digests; "
                                     "none in the data path (windows are independent, P:113, S:198)"}
     torch.cuda.set_device(local)
