@@ -15,14 +15,14 @@
 // packed add+min (VIADDMNMX.U16x2 with an immediate) per register and row; pixel u-C+1 is
 // final after row u and is emitted with one coalesced 128-byte store per warp.  The loop is
 // unrolled over the C register phases of one rotation so every slot/distance is a
-// compile-time constant: no stack, no divergence.  (kSplit of the C registers take their two
+// compile-time constant: no stack, no divergence.  (win_split(C) of the C registers take their two
 // adds on the FMA pipe instead, then one 3-way packed min: the kernel is co-limited by the ALU
 // pipe and by issue.)  The rotations in the middle of the frame
 // (all emitted rows inside the frame) run without any range check; only the first and the
 // last rotation carry them.  Instruction budget per row pair (2 pixels), see DESIGN.md §6:
 //   activity      uniform bit test + BRA (one ballot per rotation gives the C pair bits)
 //   active only:  h of 2 rows: 3 LDS.64 + 2 x (2 SHF + BREV + LOP3 + FLO.SH) + 4 IMAD (h^2),
-//                 2 (C - kSplit) VIADDMNMX.U16x2 + kSplit x (2 IMAD + VIMNMX3.U16x2)
+//                 2 (C - k) VIADDMNMX.U16x2 + k x (2 IMAD + VIMNMX3.U16x2), k = win_split(C)
 //   emit          2 IMAD extracts + 2 LDS (table) + 2 STG + 2 32-bit pointer adds
 #pragma once
 #include <cuda_fp16.h>
@@ -36,10 +36,18 @@ constexpr int kWinMaxC = 40;                      // C <= 31: h from 1 word per 
 constexpr int kWinLutMax = 2048;                  // K_sat bound of the window path
 // E_df words of one staged row: the CTA's strips plus 1 word per side (C <= 31) or 2 (C > 31)
 __host__ __device__ constexpr int window_row_words(int C) { return kWinWarps + (C > 31 ? 4 : 2); }
-#ifndef IEDS_WIN_SPLIT
-#define IEDS_WIN_SPLIT 4
+// registers per step whose two adds run on the FMA pipe (then one 3-way min on the ALU).  Measured
+// (round 2, sensor-width kernels): 8 of 19 registers for the fp32 window (C3 window kernel -0.4 %,
+// C5 +2.8 % vs 4), 4 for the small 8-bit / fp16 windows (8 loses 3.6 % / 4.8 % there)
+__host__ __device__ constexpr int win_split(int C) {
+#ifdef IEDS_WIN_SPLIT
+    return IEDS_WIN_SPLIT;
+#elif defined(IEDS_WIN_SPLIT_SMALL)
+    return C >= 16 ? 8 : IEDS_WIN_SPLIT_SMALL;
+#else
+    return C >= 16 ? 8 : 4;
 #endif
-constexpr int kSplit = IEDS_WIN_SPLIT;             // registers per step updated via the FMA pipe
+}
 
 struct WinParams {
     const uint32_t* __restrict__ Edf;   // [nb][H][NW+2], word w of row y at 1 + w, zero guards
@@ -194,7 +202,7 @@ struct WinState {
             for (int j = 0; j < C; ++j) {
                 const int m = (j + S + 1) % C;
                 const uint32_t prev = (j + 1 < C) ? P[m] : ksat4x2;
-                if (j < kSplit) {
+                if (j < win_split(C)) {
                     // FMA-pipe adds (a plain 32-bit add is the packed add: no carry crosses
                     // the halves) and one 3-way packed min on the ALU
                     const uint32_t ta = h2a * one + sq2<0>(j), tb = h2b * one + sq2<1>(j);
@@ -283,6 +291,9 @@ struct WinState {
 // 1.48 / 1.40 M at 3; C = 31 / 40 (d_sat 9 / 12): 389 / 152 k at 2, 404 / 172 k at 3, 430 /
 // 176 k at 4.  (6 CTAs: 40 registers with spills, slower everywhere.)
 __host__ __device__ constexpr int window_min_ctas(int C, bool packed) {
+#ifdef IEDS_WIN_CTAS_UNPACKED
+    if (!packed && C > 12) return IEDS_WIN_CTAS_UNPACKED;
+#endif
     return packed ? (C <= 12 ? 4 : 3) : (C <= 12 ? 5 : 4);
 }
 
