@@ -80,3 +80,25 @@ def test_ours_json_line_contract():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] == 2 * d["steps"]   # one frame + one window launch per 1000-window step
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_ours_two_ranks_code_path():
+    """The N > 1 path of our arm (`bench.py --gpus 2` relaunching under torchrun, C4 sharded,
+    cross-rank digest check), exercised on a one-GPU box: IEDS_BENCH_SHARE_GPU=1 puts both ranks
+    on cuda:0 with the gloo backend.  A code-path check only -- the numbers are not a measurement."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["IEDS_BENCH_SHARE_GPU"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--windows", "64", "--c5-windows", "32", "--no-exact", "--no-f1", "--no-c2", "--no-e2e",
+                        "--no-cpu-baseline"], capture_output=True, text=True, cwd=ROOT, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["workload"].startswith("C4")
+    assert d["config"]["windows_total"] == 64 and d["config"]["windows_per_gpu"] == 32
+    assert d["dist"]["world_size"] == 2 and d["dist"]["shared_gpu_code_path_check"] is True
+    assert d["cross_rank_check"]["match"] is True and d["cross_rank_check"]["windows_checked"] == 6
+    assert d["c5_burst"]["windows_total"] == 32 and d["c5_burst"]["scaling"] == "strong"
+    assert d["gpu_launches"] == 2 * d["steps"]
