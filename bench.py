@@ -483,25 +483,26 @@ def run_f2_stream(args, dev, world, local, wl, xy, off, nwin=200, chunk_events=1
     got = ctypes.c_int32()
     bld = ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
 
-    def run_once():
+    st = bld.stream(dt)   # created once: its device buffers are allocated outside the timed region
+
+    def run_once():   # one whole stream: push every chunk, then flush (which resets the stream)
         done = 0
-        with bld.stream(dt) as st:
-            for a in range(0, n, chunk_events):
-                b = min(n, a + chunk_events)
-                rc = lib.ieds_stream_push(st._s, t[a:].ctypes.data_as(ctypes.c_void_p),
-                                          ev[a:].ctypes.data_as(ctypes.c_void_p), b - a,
-                                          ctypes.c_void_p(hS.data_ptr()), cap, ctypes.byref(got))
-                assert rc == 0, rc
-                done += got.value
-            rc = lib.ieds_stream_flush(st._s, ctypes.c_void_p(hS.data_ptr()), cap, ctypes.byref(got))
+        for a in range(0, n, chunk_events):
+            b = min(n, a + chunk_events)
+            rc = lib.ieds_stream_push(st._s, t[a:].ctypes.data_as(ctypes.c_void_p),
+                                      ev[a:].ctypes.data_as(ctypes.c_void_p), b - a,
+                                      ctypes.c_void_p(hS.data_ptr()), cap, ctypes.byref(got))
             assert rc == 0, rc
             done += got.value
-        return done
+        rc = lib.ieds_stream_flush(st._s, ctypes.c_void_p(hS.data_ptr()), cap, ctypes.byref(got))
+        assert rc == 0, rc
+        return done + got.value
 
     run_once()
     t0 = time.perf_counter()
     done = run_once()
     el = time.perf_counter() - t0
+    st.close()
     bld.close()
     return {"metric": "streaming ingest windows/s (ieds_stream_push: host (t, xy) chunks in, host surfaces out)",
             "value": done / el, "unit": "windows/s", "windows": done, "events": n, "chunk_events": chunk_events,
@@ -949,14 +950,42 @@ def run_ours(args):
             t0 = time.perf_counter()
             bl.build_batch_host(xs, o - o[0], hS1)
             host_ms.append(1e3 * (time.perf_counter() - t0))
+        # the same call captured once in a CUDA graph (ieds_build_batch enqueues only: no host sync,
+        # no allocation) and replayed per window; the window is chosen by a 16-byte device copy of
+        # its CSR offsets into the graph's static offsets buffer
+        graph_ms = []
+        try:
+            g_off = toff[0:2].clone()
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                bl.build_batch(txy, g_off, S1)   # warm-up on the capture stream
+            cap.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                bl.build_batch(txy, g_off, S1)
+            for i in range(60):
+                k = i % nwin
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                g_off.copy_(toff[k:k + 2], non_blocking=True)
+                graph.replay()
+                torch.cuda.synchronize(dev)
+                graph_ms.append(1e3 * (time.perf_counter() - t0))
+            bl.sync()
+        except Exception as ex:   # report, never fall back
+            graph_ms = []
+            print(f"graph replay unavailable: {ex}", file=sys.stderr)
         bl.close()
         dev_ms, host_ms, gpu_ms = np.array(dev_ms[10:]), np.array(host_ms[10:]), np.array(gpu_ms[10:])
         lat = {"device_ms_p50": float(np.median(dev_ms)), "device_ms_p99": float(np.percentile(dev_ms, 99)),
+               "graph_replay_ms_p50": float(np.median(graph_ms[10:])) if graph_ms else None,
                "gpu_ms_p50": float(np.median(gpu_ms)),
                "host_e2e_ms_p50": float(np.median(host_ms)), "host_e2e_ms_p99": float(np.percentile(host_ms, 99)),
                "windows": len(dev_ms),
                "note": "one 1280x720 window per call; device_ms = wall clock of the call with its events resident, "
-                       "incl. launch + sync; gpu_ms = CUDA events around the call's kernels; host_e2e adds the H2D of "
+                       "incl. launch + sync; graph_replay_ms = the same, the call replayed from a CUDA graph; gpu_ms = CUDA "
+                       "events around the call's kernels; host_e2e adds the H2D of "
                        "its events and the D2H of its 3.7 MB surface (paper: 16.88 ms per window for the "
                        "whole pipeline incl. flow on an RTX 5000, P:555)"}
 

@@ -948,7 +948,8 @@ struct ieds_stream {
     int64_t* p_io = nullptr;     // pinned: {err, carry start}
     cudaStream_t st[2] = {nullptr, nullptr};
     cudaEvent_t kdone[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
-    void* d_S[2] = {nullptr, nullptr};   // host_chunk windows of surfaces each
+    void* d_S[2] = {nullptr, nullptr};   // `sub` windows of surfaces each
+    int sub = 0;                         // windows per build / copy-out sub-batch
 };
 
 namespace {
@@ -1015,7 +1016,7 @@ cudaError_t stream_reserve(ieds_stream* s, int64_t need) {
 int stream_build(ieds_stream* s, const uint32_t* d_xy, const int64_t* d_off, int64_t n_ev, int64_t nw, void* out) {
     ieds_handle* h = s->h;
     const size_t plane = (size_t)h->cfg.width * h->cfg.height * out_elem_bytes(h);
-    const int chunk = h->host_chunk;
+    const int chunk = s->sub;
     cudaError_t e = cudaSuccess;
     int k = 0;
     for (int64_t c0 = 0; c0 < nw; c0 += chunk, k ^= 1) {
@@ -1051,13 +1052,16 @@ int ieds_stream_create(ieds_handle* h, int64_t dt_us, ieds_stream** out) {
     ieds_stream* s = new ieds_stream();
     s->h = h;
     s->dt = dt_us;
+    // a push closes a few windows at a time: sub-batches of <= 32 windows (118 MB of fp32
+    // surfaces at 1280x720 per buffer) still overlap each copy-out with the next build
+    s->sub = std::min(h->host_chunk, 32);
     const size_t plane = (size_t)h->cfg.width * h->cfg.height * out_elem_bytes(h);
     cudaError_t e = cudaSuccess;
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
         e = cudaStreamCreateWithFlags(&s->st[i], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->kdone[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->done[i], cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaMalloc(&s->d_S[i], plane * h->host_chunk);
+        if (e == cudaSuccess) e = cudaMalloc(&s->d_S[i], plane * s->sub);
     }
     if (e == cudaSuccess) e = cudaMalloc(&s->d_err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(s->d_err, 0, sizeof(int));
