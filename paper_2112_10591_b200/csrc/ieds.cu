@@ -1123,10 +1123,10 @@ int ieds_stream_push(ieds_stream* s, const int64_t* t_us, const uint32_t* events
     if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;   // scratch shared with queued calls
     cudaError_t e = stream_reserve(s, s->n_carry + n);
     if (e == cudaSuccess && n_closed + 2 > s->cap_off) {
+        const int64_t c = std::max<int64_t>(n_closed + 2, 2 * s->cap_off + 64);   // geometric growth
         cudaFree(s->d_off);
         s->d_off = nullptr;
         s->cap_off = 0;
-        const int64_t c = std::max<int64_t>(n_closed + 2, 2 * s->cap_off + 64);
         e = cudaMalloc(&s->d_off, sizeof(int64_t) * c);
         if (e == cudaSuccess) s->cap_off = c;
     }
