@@ -844,6 +844,30 @@ def run_ours(args):
                  "kernel": "edt_kernel (uncapped exact EDT)",
                  "achieved_gbs": xe_bytes / (xe_avg / 1e3) / 1e9, "frac": xe_bytes / (xe_avg / 1e3) / 1e9 / peak,
                  "note": "IEDS_FLAG_EXACT_EDT: D2 exact everywhere (the kernel sqdist requests use)"}
+        # the sqdist request itself: surfaces + exact integer D2 written (8 B/px), default handle
+        D2 = torch.empty((nwin, H, W), dtype=torch.int32, device=dev)
+        bd = ieds.Builder(W, H, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local)
+        for _ in range(max(1, args.warmup)):
+            bd.build_batch(txy, toff, S, sqdist=D2)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        x0.record(stream)
+        for _ in range(ksteps):
+            bd.build_batch(txy, toff, S, sqdist=D2)
+        x1.record(stream)
+        torch.cuda.synchronize(dev)
+        bd.sync()
+        bd.close()
+        td = torch.tensor([x0.elapsed_time(x1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(td, op=dist.ReduceOp.MAX)
+        dms = float(td.item()) / ksteps
+        dbytes = 4.0 * n_ev + 8.0 * W * H * nwin
+        exact["sqdist"] = {"value": total_windows / (dms / 1e3), "unit": UNIT, "ms_per_step": dms,
+                           "path_gbs": dbytes / (dms / 1e3) / 1e9, "path_frac": dbytes / (dms / 1e3) / 1e9 / peak,
+                           "note": "build_batch(..., sqdist=): fp32 surface + exact uint32 D2 (4 B/event + 8 B/px)"}
+        del D2
 
     # row f1: the same workload with the epilogue variants (1 or 2 B/px written)
     def time_variant(out, transfer, odt, bpp, label, note, kernel_frac=True):
