@@ -222,8 +222,9 @@ void ieds_stream_destroy(ieds_stream *s);
  * Outputs: fwl double [num_windows] (required); var_comp, var_uncomp double [num_windows] and
  * comp_image double [num_windows][H][W] (I_comp) are optional (NULL to skip).
  * Out-of-frame events latch IEDS_ERANGE and are dropped; bad offsets latch IEDS_EORDER (both
- * reported by ieds_sync).  The handle allocates its f3 scratch (16 windows of fp64 + int32
- * images, 12 B/px) on the first call.  Enqueued on `stream`; returns IEDS_EINVAL for bad arguments. */
+ * reported by ieds_sync).  The handle allocates its f3 scratch (two sets of 16 windows of fp64 + int32
+ * images, 12 B/px: one set is re-zeroed on an internal stream while the other is used) on the
+ * first call.  Enqueued on `stream`; returns IEDS_EINVAL for bad arguments. */
 int ieds_fwl_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *events_t_us,
                    const int8_t *events_p, const int64_t *window_offsets, int64_t n_events,
                    int32_t num_windows, const float *flow, const int64_t *t_ref_us, int64_t dt_us,

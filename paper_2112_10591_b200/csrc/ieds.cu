@@ -87,9 +87,12 @@ struct ieds_handle {
     double* vtab = nullptr;    // norm_u8: [(W-1)^2 + (H-1)^2 + 1] fp64 transfer of every D2
     // row f3 scratch (allocated on the first ieds_fwl_batch): fwl_chunk windows of images
     int fwl_chunk = 0;
-    double* fwl_Ic = nullptr;             // [fwl_chunk][stride] fp64, zero between calls
-    int* fwl_Iu = nullptr;                // [fwl_chunk][stride] int32, zero between calls
-    ieds::FwlPart* fwl_part = nullptr;    // [fwl_chunk][reduce blocks] per-block partial sums
+    double* fwl_Ic[2] = {nullptr, nullptr};   // two sets of [fwl_chunk][stride] fp64 images, zero when idle
+    int* fwl_Iu[2] = {nullptr, nullptr};      // [fwl_chunk][stride] int32
+    ieds::FwlPart* fwl_part = nullptr;        // [fwl_chunk][reduce blocks] per-block partial sums
+    cudaStream_t fwl_zs = nullptr;            // re-zeroes a set while the other is splatted
+    cudaEvent_t fwl_splat[2] = {nullptr, nullptr}, fwl_zero[2] = {nullptr, nullptr};
+    int fwl_next = 0;                         // the set the next pass uses
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
     uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
@@ -647,8 +650,13 @@ void ieds_destroy(ieds_handle* h) {
     cudaFree(h->Edfs);
     cudaFree(h->dummy);
     cudaFree(h->D2n);
-    cudaFree(h->fwl_Ic);
-    cudaFree(h->fwl_Iu);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(h->fwl_Ic[i]);
+        cudaFree(h->fwl_Iu[i]);
+        if (h->fwl_splat[i]) cudaEventDestroy(h->fwl_splat[i]);
+        if (h->fwl_zero[i]) cudaEventDestroy(h->fwl_zero[i]);
+    }
+    if (h->fwl_zs) cudaStreamDestroy(h->fwl_zs);
     cudaFree(h->fwl_part);
     cudaFree(h->wmax);
     cudaFree(h->vtab);
@@ -793,24 +801,32 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     const int64_t stride = (npx + 3) & ~3ll;   // 16-byte aligned window images in the scratch
     cudaError_t e = cudaSuccess;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (!h->fwl_Ic) {
+    if (!h->fwl_Ic[0]) {
         h->fwl_chunk = kFwlChunkDefault;
         if (const char* env = std::getenv("IEDS_FWL_CHUNK")) h->fwl_chunk = std::max(1, std::min(64, std::atoi(env)));
         const int kFwlChunk = h->fwl_chunk;
-        e = cudaMalloc(&h->fwl_Ic, sizeof(double) * stride * kFwlChunk);
-        if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu, sizeof(int) * stride * kFwlChunk);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaMalloc(&h->fwl_Ic[i], sizeof(double) * stride * kFwlChunk);
+            if (e == cudaSuccess) e = cudaMalloc(&h->fwl_Iu[i], sizeof(int) * stride * kFwlChunk);
+            // zeroed on the caller's stream: a blocking cudaMemset runs on the legacy default
+            // stream, which a non-blocking caller stream does not wait for
+            if (e == cudaSuccess) e = cudaMemsetAsync(h->fwl_Ic[i], 0, sizeof(double) * stride * kFwlChunk, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(h->fwl_Iu[i], 0, sizeof(int) * stride * kFwlChunk, st);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->fwl_splat[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->fwl_zero[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(h->fwl_zero[i], st);
+        }
         if (e == cudaSuccess)
             e = cudaMalloc(&h->fwl_part, sizeof(ieds::FwlPart) * fwl_splat_blocks(kFwlChunk, h->nsm) * kFwlChunk);
-        // zeroed on the caller's stream: a blocking cudaMemset runs on the legacy default
-        // stream, which a non-blocking caller stream does not wait for
-        if (e == cudaSuccess) e = cudaMemsetAsync(h->fwl_Ic, 0, sizeof(double) * stride * kFwlChunk, st);
-        if (e == cudaSuccess) e = cudaMemsetAsync(h->fwl_Iu, 0, sizeof(int) * stride * kFwlChunk, st);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->fwl_zs, cudaStreamNonBlocking);
         if (e != cudaSuccess) {
-            cudaFree(h->fwl_Ic);
-            cudaFree(h->fwl_Iu);
+            for (int i = 0; i < 2; ++i) {
+                cudaFree(h->fwl_Ic[i]);
+                cudaFree(h->fwl_Iu[i]);
+                h->fwl_Ic[i] = nullptr;
+                h->fwl_Iu[i] = nullptr;
+            }
             cudaFree(h->fwl_part);
-            h->fwl_Ic = nullptr;
-            h->fwl_Iu = nullptr;
             h->fwl_part = nullptr;
             cudaGetLastError();
             return cuda_fail(e);
@@ -821,6 +837,8 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
     const int per_win = fwl_splat_blocks(kFwlChunk, h->nsm);
     for (int c0 = 0; c0 < num_windows; c0 += kFwlChunk) {
         const int nb = std::min(kFwlChunk, num_windows - c0);
+        const int set = h->fwl_next;
+        h->fwl_next ^= 1;
         ieds::FwlParams fp;
         fp.xy = events_xy;
         fp.t = events_t_us;
@@ -833,16 +851,22 @@ int ieds_fwl_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* eve
         fp.W = W;
         fp.H = H;
         fp.stride = stride;
-        fp.Ic = h->fwl_Ic;
-        fp.Iu = h->fwl_Iu;
+        fp.Ic = h->fwl_Ic[set];
+        fp.Iu = h->fwl_Iu[set];
         fp.err = h->err;
+        // this set was re-zeroed on the side stream after its last pass
+        cudaError_t ce = cudaStreamWaitEvent(st, h->fwl_zero[set], 0);
+        if (ce != cudaSuccess) return IEDS_ECUDA;
         ieds::fwl_splat_kernel<<<dim3(per_win, nb), ieds::kFwlThreads, 0, st>>>(fp, h->fwl_part);
-        cudaError_t ce = cudaSuccess;
         if (comp_image)
-            ce = cudaMemcpy2DAsync(comp_image + (size_t)c0 * npx, sizeof(double) * npx, h->fwl_Ic, sizeof(double) * stride,
-                                   sizeof(double) * npx, nb, cudaMemcpyDeviceToDevice, st);
-        if (ce == cudaSuccess) ce = cudaMemsetAsync(h->fwl_Ic, 0, sizeof(double) * stride * nb, st);   // zero for the next windows
-        if (ce == cudaSuccess) ce = cudaMemsetAsync(h->fwl_Iu, 0, sizeof(int) * stride * nb, st);
+            ce = cudaMemcpy2DAsync(comp_image + (size_t)c0 * npx, sizeof(double) * npx, h->fwl_Ic[set],
+                                   sizeof(double) * stride, sizeof(double) * npx, nb, cudaMemcpyDeviceToDevice, st);
+        // re-zero the set for its next pass on the side stream, overlapped with the next splat
+        if (ce == cudaSuccess) ce = cudaEventRecord(h->fwl_splat[set], st);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(h->fwl_zs, h->fwl_splat[set], 0);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(h->fwl_Ic[set], 0, sizeof(double) * stride * nb, h->fwl_zs);
+        if (ce == cudaSuccess) ce = cudaMemsetAsync(h->fwl_Iu[set], 0, sizeof(int) * stride * nb, h->fwl_zs);
+        if (ce == cudaSuccess) ce = cudaEventRecord(h->fwl_zero[set], h->fwl_zs);
         if (ce != cudaSuccess) return IEDS_ECUDA;
         ieds::fwl_finalize_kernel<<<nb, ieds::kFwlThreads, 0, st>>>(h->fwl_part, per_win, npx, fwl + c0,
                                                                      var_comp ? var_comp + c0 : nullptr,

@@ -172,3 +172,25 @@ def test_fwl_first_call_on_a_side_stream():
         sl = slice(off[b], off[b + 1])
         ref = oracle.fwl(xy[sl], t[sl], p[sl], DAVIS.width, DAVIS.height, flows[b], t_ref[b], DAVIS.dt_us)["fwl"]
         assert abs(g[b] - ref) <= 1e-9 * abs(ref)
+
+
+def test_fwl_scratch_sets_alternate_across_passes_and_calls():
+    """The f3 scratch is two image sets, one re-zeroed on an internal stream while the other is
+    splatted: 3 calls of 37 windows (3 passes of <= 16 windows each) must all equal the oracle,
+    so every pass starts from zeroed images whichever set and call it falls in."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    dev = torch.device("cuda", 0)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    with ieds.Builder(DAVIS.width, DAVIS.height, 1, 4, device=0) as bld:
+        for call in range(3):
+            xy, t, p, off, flows, _fl, t_ref = flow_batch(DAVIS, 5 + call, 0, 37)
+            r = bld.fwl_batch(T(xy.view(np.int32)), T(t), T(p), T(off), T(flows), T(t_ref), DAVIS.dt_us)
+            bld.sync()
+            g = r["fwl"].cpu().numpy()
+            for b in (0, 15, 16, 31, 32, 36):
+                sl = slice(off[b], off[b + 1])
+                ref = oracle.fwl(xy[sl], t[sl], p[sl], DAVIS.width, DAVIS.height, flows[b], t_ref[b], DAVIS.dt_us)["fwl"]
+                assert abs(g[b] - ref) <= 1e-9 * abs(ref), (call, b)
