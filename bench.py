@@ -237,6 +237,30 @@ def resolve_config(args, world: int) -> str:
     return "C4" if world > 1 else "C3"
 
 
+def workload_config(name: str, world: int, rank: int, windows: int = 0, events_per_gpu=None) -> dict:
+    """The line's `config` for workload `name` at this world size: the same dict in both arms, so
+    the reference arm reports exactly our arm's config (its bounded per-step sample is stated in
+    its cpu_baseline.sample and reference_windows_per_step)."""
+    wl = WORKLOADS[name]
+    c = wl.scene
+    strong = name == "C4"
+    if strong:
+        total = windows or wl.n_windows
+        nwin = len(shard(total, world, rank))
+    else:
+        nwin = windows or wl.n_windows
+        total = nwin * world
+    n_ev = events_per_gpu if events_per_gpu is not None else c.events_per_window * nwin
+    return {"workload": (f"{wl.name}: {c.width}x{c.height} Gen4-like, {total} windows sharded over {world} GPU(s), "
+                         if strong else f"{wl.name}: {c.width}x{c.height} Gen4-like, {nwin} windows per GPU, ")
+                        + f"{c.events_per_window} events per window",
+            "windows_total": total, "windows_per_gpu": nwin, "events_per_gpu": int(n_ev), "width": c.width,
+            "height": c.height, "n_d": wl.n_d, "n_f": wl.n_f, "d_sat": wl.d_sat,
+            "alpha": wl.d_sat / math.log(255.0),   # Eq. (2)-(3), P:228-233
+            "l2": "inputs+outputs larger than L2 (events %.0f MB, surfaces %.0f MB per step)" % (
+                4 * n_ev / 1e6, 4 * c.width * c.height * nwin / 1e6)}
+
+
 _REF_EVENTS = []   # the reference arm's pre-generated windows (inherited by the forked workers)
 
 
@@ -285,10 +309,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if name == "C4" else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{wl.name}: {c.width}x{c.height}, {c.events_per_window} events/window "
-                               f"({per_step} windows per step)",
-                   "windows_per_step": per_step, "width": c.width, "height": c.height, "n_d": wl.n_d,
-                   "n_f": wl.n_f, "d_sat": wl.d_sat},
+        "config": workload_config(name, world, 0, args.windows),
+        "reference_windows_per_step": per_step,
         "mev_per_s": value * c.events_per_window / 1e6,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu": cpu_model(), "kind": "oracle",
                          "sample": f"each step: {per_step} distinct windows of {wl.name}, one process per core, "
@@ -1032,13 +1054,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u32+i32+f32", "data": "synthetic",
-        "config": {"workload": (f"{wl.name}: {W}x{H} Gen4-like, {total_windows} windows sharded over {world} GPU(s), "
-                                if strong else f"{wl.name}: {W}x{H} Gen4-like, {nwin} windows per GPU, ")
-                               + f"{c.events_per_window} events per window",
-                   "windows_total": total_windows, "windows_per_gpu": nwin, "events_per_gpu": n_ev, "width": W, "height": H, "n_d": wl.n_d,
-                   "n_f": wl.n_f, "d_sat": wl.d_sat, "alpha": bld.params.alpha,
-                   "l2": "inputs+outputs larger than L2 (events %.0f MB, surfaces %.0f MB per step)" % (
-                       4 * n_ev / 1e6, 4 * W * H * nwin / 1e6)},
+        "config": workload_config(name, world, 0, args.windows, events_per_gpu=n_ev),
         "mev_per_s": value * (n_ev / nwin) / 1e6,
         "hbm_frac_path": {"achieved_gbs": path_gbs, "peak": peak, "frac": path_gbs / peak,
                           "frac_nominal_8tbs": path_gbs / 8000.0,

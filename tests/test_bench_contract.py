@@ -30,6 +30,13 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
     assert d["vs_baseline"] is None and d["data"] == "synthetic"
     assert d["config"]["workload"].startswith("C3")
+    # the reference arm reports our arm's config for the same world size (the driver compares them)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert d["config"] == bench.workload_config("C3", 1, 0)
+    assert d["reference_windows_per_step"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["value"] == d["value"] and cb["cores"] >= 1 and cb["sample"]
