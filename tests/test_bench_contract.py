@@ -86,6 +86,13 @@ def test_ours_json_line_contract():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] == 2 * d["steps"]   # one frame + one window launch per 1000-window step
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    # the reference arm reports this same config (test_reference_arm_json_line)
+    assert d["config"] == bench.workload_config("C3", 1, 0, events_per_gpu=d["config"]["events_per_gpu"])
+    assert d["config"]["events_per_gpu"] == 75_000_000
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
 
