@@ -352,6 +352,83 @@ def cycled_batch(name, k0, nwin, pool, dev):
     return txy, torch.from_numpy(off).to(dev), int(off[-1]), pool
 
 
+def run_weak_c3(args, dev, stream, world, local, peak, txy, off, n):
+    """Weak scaling at N > 1: each rank builds the first n windows of its resident C4 shard (C3's
+    per-GPU batch shape), timed like the main line, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_10591_b200 as ieds
+
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    toff = torch.from_numpy(np.ascontiguousarray(off[:n + 1])).to(dev)
+    S = torch.empty((n, c.height, c.width), dtype=torch.float32, device=dev)
+    with ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=local) as bld:
+        for _ in range(max(1, args.warmup)):
+            bld.build_batch(txy, toff, S)
+        ksteps = max(1, min(args.steps, 10))
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ksteps):
+            bld.build_batch(txy, toff, S)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        bld.sync()
+    tm = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item()) / ksteps
+    del S
+    return {"workload": f"C3 per GPU: {n} windows on each of {world} GPUs (first windows of each rank's C4 shard)",
+            "windows_total": n * world, "windows_per_gpu": n, "scaling": "weak",
+            "value": n * world / (ms / 1e3), "unit": "surfaces/s", "ms_per_step": ms, "steps": ksteps}
+
+
+def run_c4_single(args, dev, stream, peak, xy, off, total=16000):
+    """C4 (BASELINE configs[3]: 16,000 1280x720 windows) on one GPU -- the R = 1 point of its
+    strong-scaling curve -- with the events of the 1000 resident C3 windows cycled 16 times."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    wl = WORKLOADS["C4"]
+    c = wl.scene
+    pool = len(off) - 1
+    reps, rem = divmod(total, pool)
+    txy_pool = torch.from_numpy(xy.view(np.int32)).to(dev)
+    txy = torch.cat([txy_pool] * reps + ([txy_pool[:int(off[rem])]] if rem else []))
+    lens = np.diff(off)
+    o = np.zeros(total + 1, np.int64)
+    o[1:] = np.cumsum(np.concatenate([np.tile(lens, reps), lens[:rem]]))
+    toff = torch.from_numpy(o).to(dev)
+    S = torch.empty((total, c.height, c.width), dtype=torch.float32, device=dev)
+    with ieds.Builder(c.width, c.height, wl.n_d, wl.n_f, d_sat=wl.d_sat, device=dev.index) as bld:
+        for _ in range(max(1, args.warmup)):
+            bld.build_batch(txy, toff, S)
+        ksteps = max(1, min(args.steps, 5))
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ksteps):
+            bld.build_batch(txy, toff, S)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        bld.sync()
+    ms = e0.elapsed_time(e1) / ksteps
+    n_ev = int(o[-1])
+    bytes_step = 4.0 * n_ev + 4.0 * c.width * c.height * total + 8.0 * (total + 1)
+    del S, txy, toff
+    return {"workload": f"C4: 1280x720, {total} windows on 1 GPU (R = 1), 75000 events per window",
+            "windows_total": total, "distinct_windows": pool, "scaling": "strong", "value": total / (ms / 1e3),
+            "unit": "surfaces/s", "ms_per_step": ms, "steps": ksteps,
+            "hbm_frac_path": bytes_step / (ms / 1e3) / 1e9 / peak,
+            "note": "the R = 1 baseline of BASELINE's C4 strong scaling; N > 1 runs report C4 as the main line"}
+
+
 def run_config_brief(args, name, dev, stream, world, local, peak, nwin=None, total=None, pool=None):
     """Another §8(d) workload (C2: 346x260; C5: the 1280x720 dense burst) on the same device:
     surfaces/s and the whole-path HBM fraction over a few steps, inputs resident (not the
@@ -953,6 +1030,18 @@ def run_ours(args):
     if not args.no_c2 and name != "C2":
         c2 = run_config_brief(args, "C2", dev, stream, world, local, peak, pool=2000)
 
+    # BASELINE's C4 at R = 1 ("16,000 windows ... plus R=1 baseline"): at N = 1 the
+    # main line is C3, so the 16,000-window batch is timed here on the one GPU, its events cycling
+    # through the 1000 generated C3 windows (300 MB > L2); at N > 1 C4 is the main line itself
+    c4_r1 = None
+    if not args.no_c4_r1 and world == 1 and name == "C3":
+        c4_r1 = run_c4_single(args, dev, stream, peak, xy, off)
+    # and at N > 1 the weak-scaling view of the same path: every rank builds 1000 windows of its
+    # resident shard (C3's per-GPU batch), value = all ranks' windows / the slowest rank's time
+    c3_weak = None
+    if world > 1 and name == "C4" and nwin >= 1:
+        c3_weak = run_weak_c3(args, dev, stream, world, local, peak, txy, off, min(nwin, 1000))
+
     # the dense burst config at BASELINE's shape (configs[4]: 300k events per 1280x720 window,
     # fill 13 %; 16,000 windows sharded across the ranks; 256 distinct windows per GPU, cycled)
     c5 = None
@@ -1089,6 +1178,8 @@ def run_ours(args):
         "f4_flow": f4,
         "c2_lowres": c2,
         "c5_burst": c5,
+        "c4_r1_baseline": c4_r1,
+        "c3_weak_scaling": c3_weak,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -1119,6 +1210,7 @@ def main():
     ap.add_argument("--no-f4", action="store_true", help="skip the flow consumer (row f4) run")
     ap.add_argument("--no-c2", action="store_true", help="skip the low-resolution C2 run")
     ap.add_argument("--no-c5", action="store_true", help="skip the dense-burst C5 run")
+    ap.add_argument("--no-c4-r1", action="store_true", help="skip the one-GPU 16k-window C4 run (N = 1)")
     ap.add_argument("--f3-windows", type=int, default=128, help="C3-geometry windows of the FWL (row f3) run")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-window latency (row f2) run")
     ap.add_argument("--chunk", type=int, default=0, help="windows per launch pair (0 = library default)")

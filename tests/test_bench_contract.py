@@ -72,7 +72,7 @@ def test_reference_arm_other_ranks_exit_quietly():
 def test_ours_json_line_contract():
     """Our arm's line carries every key of the driver contract (short run, rows skipped)."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3", "--no-exact",
-                        "--no-f1", "--no-f3", "--no-f4", "--no-c2", "--no-c5", "--no-latency"],
+                        "--no-f1", "--no-f3", "--no-f4", "--no-c2", "--no-c5", "--no-c4-r1", "--no-latency"],
                        capture_output=True, text=True, cwd=ROOT, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
@@ -115,4 +115,5 @@ def test_ours_two_ranks_code_path():
     assert d["dist"]["world_size"] == 2 and d["dist"]["shared_gpu_code_path_check"] is True
     assert d["cross_rank_check"]["match"] is True and d["cross_rank_check"]["windows_checked"] == 6
     assert d["c5_burst"]["windows_total"] == 32 and d["c5_burst"]["scaling"] == "strong"
+    assert d["c3_weak_scaling"]["scaling"] == "weak" and d["c3_weak_scaling"]["windows_per_gpu"] == 32
     assert d["gpu_launches"] == 2 * d["steps"]
