@@ -230,9 +230,31 @@ struct WinState {
 
     // A rotation with no site in reach while every slot is still saturated (4 K_sat): its 2C
     // rows are the saturated value and the slots stay as they are -- store them directly.
+    // sensor-width 8-bit / fp16 path: the warp's 2C x 32 outputs as 16-byte stores (the strip's
+    // rows are 16-byte aligned: W * sizeof(OutT) % 16 == 0), 16 / sizeof(OutT) rows per store
+    template <int K = 0>
+    __device__ __forceinline__ void saturated_rows_v4(uint64_t base, uint32_t rep) {
+        constexpr int LPR = 2 * (int)sizeof(OutT);   // lanes per row (16 bytes each)
+        constexpr int RPI = 32 / LPR;                // rows per store instruction
+        if constexpr (K * RPI < 2 * C) {
+            if (K * RPI + lane / LPR < 2 * C) {
+                asm volatile("st.global.cs.v4.b32 [%0+%1], {%2, %2, %2, %2};" ::"l"(base),
+                             "n"(K * RPI * WIDTH * (int)sizeof(OutT)), "r"(rep) : "memory");
+            }
+            saturated_rows_v4<K + 1>(base, rep);
+        }
+    }
+
     template <int R = 0>
     __device__ __forceinline__ void saturated_rows(uint32_t bits) {
-        if constexpr (R < 2 * C) {
+        if constexpr (WIDTH > 0 && sizeof(OutT) < 4 && R == 0) {
+            constexpr int LPR = 2 * (int)sizeof(OutT);
+            const uint32_t rep = sizeof(OutT) == 1 ? bits * 0x01010101u : bits * 0x00010001u;
+            const uint64_t base = op - (uint64_t)(lane * sizeof(OutT)) +
+                                  (uint64_t)(lane / LPR) * (WIDTH * sizeof(OutT)) + (uint64_t)(lane % LPR) * 16u;
+            saturated_rows_v4(base, rep);
+            op += (uint64_t)(2 * C) * wb;
+        } else if constexpr (R < 2 * C) {
             if constexpr (WIDTH > 0) {
                 st_cs_bits_at<R * WIDTH * (int)sizeof(OutT)>(static_cast<OutT*>(nullptr), op, bits);
             } else {
