@@ -89,9 +89,6 @@ __device__ __forceinline__ uint32_t denoised_word(const uint32_t* fr, const Fram
 // nonzero if the event is outside the frame.  Branch-free: the coordinates are clamped into the
 // frame with one packed min (lim = (H-1) << 16 | (W-1)), the row into the band, and an event
 // outside either ORs nothing.
-#ifndef IEDS_SCATTER_TEST
-#define IEDS_SCATTER_TEST 0
-#endif
 template <bool BANDED>
 __device__ __forceinline__ uint32_t scatter_event(uint32_t* fr1, uint32_t lim, int NWP, int ya, int yb, uint32_t v) {
     const uint32_t c = __vminu2(v, lim);
@@ -100,14 +97,7 @@ __device__ __forceinline__ uint32_t scatter_event(uint32_t* fr1, uint32_t lim, i
         const int yc = min(max(y, ya), yb);
         atomicOr(&fr1[yc * NWP + (x >> 5)], (c == v && yc == y) ? 1u << (x & 31) : 0u);
     } else {   // one band holds every row
-#if IEDS_SCATTER_TEST
-        // duplicates (2.3 events per pixel at C3, 4.9 at C5) skip the atomic when the bit is set
-        uint32_t* a = &fr1[y * NWP + (x >> 5)];
-        const uint32_t bit = c == v ? 1u << (x & 31) : 0u;
-        if (bit & ~*reinterpret_cast<volatile uint32_t*>(a)) atomicOr(a, bit);
-#else
         atomicOr(&fr1[y * NWP + (x >> 5)], c == v ? 1u << (x & 31) : 0u);
-#endif
     }
     return c ^ v;
 }
