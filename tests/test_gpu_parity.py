@@ -270,6 +270,32 @@ def test_full_size_bench_config_sampled():
         assert np.all((Sh[i] == 0) == (refs[i]["E_df"] == 1))
 
 
+def test_c5_bulk_launch_sampled():
+    """C5 (the dense burst, 300k events per window) in the bench's bulk launch configuration: 296
+    windows (two waves of frame CTAs, so the events of the next wave are L2-prefetched, capped per
+    window) cycling 12 generated windows, sampled against the oracle; surfaces also bit-identical
+    to the exact-EDT kernel's."""
+    torch = _torch()
+    wl = WORKLOADS["C5"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy0, off0 = batch_events(c, wl.seed, 100, 12)
+    ws = [xy0[off0[i % 12]:off0[i % 12 + 1]] for i in range(296)]
+    xy, off = csr(ws)
+    dev = torch.device("cuda", 0)
+    txy, toff = torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev)
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0) as bld:
+        S = bld.build_batch(txy, toff)
+        bld.sync()
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0, exact_edt=True) as bx:
+        Sx = bx.build_batch(txy, toff)
+        bx.sync()
+    assert torch.equal(S, Sx)
+    for b in (0, 5, 147, 148, 150, 295):
+        ref = oracle.build_window(ws[b], c.width, c.height, wl.n_d, wl.n_f, a, want=("S",))["S"]
+        assert np.abs(S[b].cpu().numpy().astype(np.float64) - ref).max() <= TOL, b
+
+
 # ----------------------------------------------------------------------------- streaming vs exact
 
 def _stress_windows(W, H, seed):

@@ -105,3 +105,39 @@ def test_random_epilogue_variants(seed):
                 fin = np.isfinite(e16)
                 ulp = np.spacing(np.abs(e16[fin])).astype(np.float64)
                 assert np.all(np.abs(S[b][fin].astype(np.float64) - e16[fin].astype(np.float64)) <= ulp)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_sensor_width_configs(seed):
+    """The 1280-wide sensor instantiations (compile-time row stride, immediate-offset stores; the
+    8-bit / fp16 saturated-rotation path) on random heights, thresholds, densities, batch sizes
+    (row-band latency shape and bulk shape) and output formats: bit-identical to the exact-EDT
+    kernel's surfaces, and the fp32 ones within 2e-6 of the oracle on sampled windows."""
+    import torch
+
+    import paper_2112_10591_b200 as ieds
+
+    rng = np.random.default_rng(7000 + seed)
+    W = 1280
+    H = int(rng.choice([1, 2, 37, 38, 39, 76, 200, 720]) if rng.random() < 0.5 else rng.integers(1, 721))
+    n_d, n_f = int(rng.integers(0, 5)), int(rng.integers(1, 6))
+    out = str(rng.choice(["f32", "u8", "f16"]))
+    nwin = int(rng.choice([1, 3, 160]))
+    dens = [0.0, 0.0003, 0.002, 0.01, 0.05, 0.3]
+    distinct = [random_frame_events(W, H, float(rng.choice(dens)), 31 * seed + i) for i in range(4)]
+    wins = [distinct[i % 4] for i in range(nwin)]
+    xy, off = csr(wins)
+    dev = torch.device("cuda", 0)
+    txy = torch.from_numpy(np.ascontiguousarray(xy).view(np.int32)).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    res = {}
+    for exact in (False, True):
+        with ieds.Builder(W, H, n_d, n_f, d_sat=6.0, device=0, out=out, exact_edt=exact) as bld:
+            res[exact] = bld.build_batch(txy, toff).cpu().numpy()
+            bld.sync()
+    assert np.array_equal(res[False].view(np.uint8), res[True].view(np.uint8)), (H, n_d, n_f, out, nwin)
+    if out == "f32":
+        a = oracle.alpha_from_dsat(6.0)
+        for b in sorted({0, nwin - 1}):
+            ref = oracle.build_window(wins[b], W, H, n_d, n_f, a, want=("S",))["S"]
+            assert np.abs(res[False][b].astype(np.float64) - ref).max() <= 2e-6
