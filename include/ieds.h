@@ -274,6 +274,36 @@ int ieds_flow_step(ieds_flow_handle *h, const float *surface, const uint32_t *ed
 /* Kernel launches of one non-first step (inside and outside its graph). */
 int64_t ieds_flow_launches_per_step(const ieds_flow_handle *h);
 
+/* ---- The Fig. 1 pipeline: events in, flow out (rows f2 + a1-a5 + f4) ---------
+ * The paper's blocks -- accumulation, denoising and filling, IEDS, flow -- run concurrently, the
+ * image of a window being built "when the time window has expired".  An ieds_pipeline
+ * takes host chunks of a live stream like ieds_stream_push, builds each closed window's surface
+ * and denoised edge bits (handle h), and runs the flow consumer (handle f, same width and height)
+ * on them in window order: the surfaces of the next sub-batch of closed windows are built on one
+ * internal stream while the flow of the previous ones runs on another, and each window's flow is
+ * copied out while the next window's flow is computed.  Results are bit-identical to
+ * ieds_stream_push followed by ieds_flow_step per window (tests/test_gpu_pipeline.py).
+ * Outputs (HOST, may be NULL): flow float32 [max_out][H][W][2], valid uint8 [max_out][H][W],
+ * surfaces [max_out][H][W] of h's output type (which must be IEDS_OUT_F32, the flow's input).
+ * The pipeline borrows h and f (destroy it first); flush also resets f (a new sequence). */
+typedef struct ieds_pipeline ieds_pipeline;
+
+int ieds_pipeline_create(ieds_handle *h, ieds_flow_handle *f, int64_t dt_us, ieds_pipeline **out);
+
+/* Windows a push of [t_first_us, t_last_us] would close (as ieds_stream_closing). */
+int64_t ieds_pipeline_closing(const ieds_pipeline *p, int64_t t_first_us, int64_t t_last_us);
+
+/* As ieds_stream_push; for every closed window writes its flow / valid / surface outputs. */
+int ieds_pipeline_push(ieds_pipeline *p, const int64_t *t_us, const uint32_t *events_xy, int64_t n,
+                       float *flow, uint8_t *valid, void *surfaces, int32_t max_out, int32_t *num_out);
+
+/* End of stream: the open window's outputs (1 window, or 0), then the stream and f are reset. */
+int ieds_pipeline_flush(ieds_pipeline *p, float *flow, uint8_t *valid, void *surfaces, int32_t max_out,
+                        int32_t *num_out);
+
+/* NULL-safe. */
+void ieds_pipeline_destroy(ieds_pipeline *p);
+
 /* Wait for `stream`, then return (and clear) the latched device error, or IEDS_OK. */
 int ieds_sync(ieds_handle *h, void *stream);
 

@@ -13,7 +13,7 @@ import dataclasses
 from ._lib import (IedsFlowConfig, IEDS_FLAG_EXACT_EDT, IEDS_NO_EDGE, OUT_FORMATS, TRANSFERS, IedsConfig, IedsError, IedsOrderError, IedsRangeError, LIB_PATH,
                    check, load)
 
-__all__ = ["Builder", "EventStream", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
+__all__ = ["Builder", "EventStream", "Pipeline", "alpha_from_dsat", "version", "IedsError", "IedsRangeError", "IedsOrderError",
            "IEDS_NO_EDGE", "LIB_PATH"]
 
 load()   # fail loudly at import if libieds.so is missing
@@ -319,6 +319,78 @@ class EventStream:
         if getattr(self, "_s", None) is not None and self._s.value:
             load().ieds_stream_destroy(self._s)
             self._s = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class Pipeline:
+    """The Fig. 1 pipeline (ieds_pipeline_*): host chunks of a live event stream in,
+    per closed window its flow (and valid mask, optionally its surface) out, the surfaces of later
+    windows built while earlier windows' flow runs.  push(t_us, xy) -> dict of host arrays
+    {"flow": float32 [k, H, W, 2], "valid": uint8 [k, H, W], "surfaces": float32 [k, H, W] if
+    asked}; flush() closes the last window and starts a new sequence (stream and estimator)."""
+
+    def __init__(self, builder: "Builder", estimator: "FlowEstimator", dt_us: int, surfaces: bool = False):
+        self.builder, self.estimator = builder, estimator
+        self.want_surfaces = surfaces
+        self._p = ctypes.c_void_p()
+        check(load().ieds_pipeline_create(builder._h, estimator._h, int(dt_us), ctypes.byref(self._p)),
+              "ieds_pipeline_create")
+
+    def closing(self, t_first_us: int, t_last_us: int) -> int:
+        return int(load().ieds_pipeline_closing(self._p, int(t_first_us), int(t_last_us)))
+
+    def _outs(self, k):
+        import numpy as np
+
+        H, W = self.builder.height, self.builder.width
+        o = {"flow": np.empty((k, H, W, 2), np.float32), "valid": np.empty((k, H, W), np.uint8)}
+        if self.want_surfaces:
+            o["surfaces"] = np.empty((k, H, W), np.float32)
+        return o
+
+    @staticmethod
+    def _ptrs(o):
+        return [o[k].ctypes.data_as(ctypes.c_void_p) if k in o else None for k in ("flow", "valid", "surfaces")]
+
+    def push(self, t_us, events_xy) -> dict:
+        import numpy as np
+
+        if hasattr(t_us, "numpy"):
+            t_us = t_us.numpy()
+        if hasattr(events_xy, "numpy"):
+            events_xy = events_xy.numpy()
+        t = np.ascontiguousarray(t_us, dtype=np.int64)
+        xy = np.ascontiguousarray(events_xy).view(np.uint32)
+        if t.shape != xy.shape or t.ndim != 1:
+            raise ValueError("t_us and events_xy must be 1-D arrays of the same length")
+        n = len(t)
+        o = self._outs(self.closing(int(t[0]), int(t[-1])) if n else 0)
+        got = ctypes.c_int32()
+        check(load().ieds_pipeline_push(self._p, t.ctypes.data_as(ctypes.c_void_p), xy.ctypes.data_as(ctypes.c_void_p),
+                                        n, *self._ptrs(o), len(o["flow"]), ctypes.byref(got)), "ieds_pipeline_push")
+        return {k: v[:got.value] for k, v in o.items()}
+
+    def flush(self) -> dict:
+        o = self._outs(1)
+        got = ctypes.c_int32()
+        check(load().ieds_pipeline_flush(self._p, *self._ptrs(o), 1, ctypes.byref(got)), "ieds_pipeline_flush")
+        return {k: v[:got.value] for k, v in o.items()}
+
+    def close(self):
+        if getattr(self, "_p", None) is not None and self._p.value:
+            load().ieds_pipeline_destroy(self._p)
+            self._p = ctypes.c_void_p()
 
     def __del__(self):
         try:

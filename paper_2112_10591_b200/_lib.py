@@ -25,7 +25,8 @@ IEDS_NO_EDGE = 0xFFFFFFFF
 EXPORTS = (
     "ieds_create", "ieds_destroy", "ieds_build_batch", "ieds_build_batch_host", "ieds_sync",
     "ieds_window_offsets", "ieds_window_count", "ieds_stream_create", "ieds_stream_closing", "ieds_stream_push",
-    "ieds_stream_flush", "ieds_stream_destroy", "ieds_fwl_batch", "ieds_flow_create", "ieds_flow_destroy", "ieds_flow_reset",
+    "ieds_stream_flush", "ieds_stream_destroy", "ieds_pipeline_create", "ieds_pipeline_closing", "ieds_pipeline_push",
+    "ieds_pipeline_flush", "ieds_pipeline_destroy", "ieds_fwl_batch", "ieds_flow_create", "ieds_flow_destroy", "ieds_flow_reset",
     "ieds_flow_step", "ieds_flow_launches_per_step", "ieds_launches_per_batch", "ieds_profile_enable", "ieds_profile_read", "ieds_strerror", "ieds_alpha_from_dsat", "ieds_version",
 )
 
@@ -115,6 +116,16 @@ def load():
     lib.ieds_stream_flush.restype = ctypes.c_int
     lib.ieds_stream_destroy.argtypes = [P]
     lib.ieds_stream_destroy.restype = None
+    lib.ieds_pipeline_create.argtypes = [P, P, i64, ctypes.POINTER(P)]
+    lib.ieds_pipeline_create.restype = ctypes.c_int
+    lib.ieds_pipeline_closing.argtypes = [P, i64, i64]
+    lib.ieds_pipeline_closing.restype = i64
+    lib.ieds_pipeline_push.argtypes = [P, P, P, i64, P, P, P, i32, ctypes.POINTER(i32)]
+    lib.ieds_pipeline_push.restype = ctypes.c_int
+    lib.ieds_pipeline_flush.argtypes = [P, P, P, P, i32, ctypes.POINTER(i32)]
+    lib.ieds_pipeline_flush.restype = ctypes.c_int
+    lib.ieds_pipeline_destroy.argtypes = [P]
+    lib.ieds_pipeline_destroy.restype = None
     lib.ieds_fwl_batch.argtypes = [P, P, P, P, P, i64, i32, P, P, i64, P, P, P, P, P]
     lib.ieds_fwl_batch.restype = ctypes.c_int
     lib.ieds_flow_create.argtypes = [P, P]

@@ -498,3 +498,14 @@ int64_t ieds_flow_launches_per_step(const ieds_flow_handle* h) {
 }
 
 }  // extern "C"
+
+namespace ieds {
+// geometry and device of a flow handle, for the pipeline in ieds.cu (not part of the C ABI)
+int flow_dims(const ieds_flow_handle* h, int* width, int* height, int* device) {
+    if (!h) return IEDS_EINVAL;
+    *width = h->cfg.width;
+    *height = h->cfg.height;
+    *device = h->dev;
+    return IEDS_OK;
+}
+}  // namespace ieds

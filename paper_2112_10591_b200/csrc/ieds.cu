@@ -1126,15 +1126,21 @@ int64_t ieds_stream_closing(const ieds_stream* s, int64_t t_first_us, int64_t t_
     return std::max<int64_t>(0, (t_last_us - t0) / s->dt - (s->started ? s->k_open : 0));
 }
 
-int ieds_stream_push(ieds_stream* s, const int64_t* t_us, const uint32_t* events_xy, int64_t n, void* surfaces,
-                     int32_t max_out, int32_t* num_out) {
-    if (!s || !num_out || n < 0 || max_out < 0) return IEDS_EINVAL;
-    *num_out = 0;
-    if (n == 0) return IEDS_OK;
-    if (!t_us || !events_xy) return IEDS_EINVAL;
+}  // extern "C"
+
+namespace {
+
+// A staged push: the chunk appended after the carry on the device, the boundaries of the windows it
+// closes in s->d_off (n_closed of them from offsets[0]), the still-open window from `carry0` on.
+// Nothing of the stream's state is changed until stream_commit.
+struct StreamIngest {
+    int64_t t0 = 0, k_last = 0, n_closed = 0, n_tot = 0, carry0 = 0, last_t = 0;
+    int cur = 0;
+};
+
+int stream_ingest(ieds_stream* s, const int64_t* t_us, const uint32_t* events_xy, int64_t n, int32_t max_out,
+                  StreamIngest* ing) {
     ieds_handle* h = s->h;
-    DeviceGuard g(h->dev);
-    if (!g.ok) return IEDS_ECUDA;
     // host-checkable order: the chunk continues the stream and its ends are ordered (the
     // device kernel checks every adjacent pair below, before anything is built)
     if ((s->started && t_us[0] < s->last_t) || t_us[n - 1] < t_us[0]) return IEDS_EORDER;
@@ -1143,7 +1149,6 @@ int ieds_stream_push(ieds_stream* s, const int64_t* t_us, const uint32_t* events
     const int64_t k_last = (t_us[n - 1] - t0) / s->dt;
     const int64_t n_closed = k_last - k_open;
     if (n_closed > max_out) return IEDS_ECAPACITY;
-    if (n_closed > 0 && !surfaces) return IEDS_EINVAL;
     if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;   // scratch shared with queued calls
     cudaError_t e = stream_reserve(s, s->n_carry + n);
     if (e == cudaSuccess && n_closed + 2 > s->cap_off) {
@@ -1196,29 +1201,81 @@ int ieds_stream_push(ieds_stream* s, const int64_t* t_us, const uint32_t* events
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return IEDS_ECUDA;
     if (*reinterpret_cast<int*>(&s->p_io[0]) & ieds::kErrOrder) return IEDS_EORDER;   // rejected, stream unchanged
-    const int64_t carry0 = s->p_io[1];
-    int rc = IEDS_OK;
-    if (n_closed > 0) {
-        e = cudaEventRecord(s->kdone[1], st);   // the first sub-batch waits for the offsets
-        if (e != cudaSuccess) return cuda_fail(e);
-        rc = stream_build(s, s->d_xy[cur], s->d_off, n_tot, n_closed, surfaces);
-        if (rc != IEDS_OK) return rc;
-    }
-    // the open window k_last (events [carry0, n_tot)) moves to the front of the other buffer
-    const int nxt = cur ^ 1;
-    const int64_t nc = n_tot - carry0;
-    e = cudaMemcpyAsync(s->d_xy[nxt], s->d_xy[cur] + carry0, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, st);
+    ing->t0 = t0;
+    ing->k_last = k_last;
+    ing->n_closed = n_closed;
+    ing->n_tot = n_tot;
+    ing->carry0 = s->p_io[1];
+    ing->last_t = t_us[n - 1];
+    ing->cur = cur;
+    // the first sub-batch of the closed windows waits for the offsets
+    e = cudaEventRecord(s->kdone[1], st);
+    return e == cudaSuccess ? IEDS_OK : cuda_fail(e);
+}
+
+// the open window k_last (events [carry0, n_tot)) moves to the front of the other buffer, and the
+// stream's state advances (enqueued on st[0]; the caller synchronises)
+int stream_commit(ieds_stream* s, const StreamIngest& ing) {
+    cudaStream_t st = s->st[0];
+    const int cur = ing.cur, nxt = cur ^ 1;
+    const int64_t nc = ing.n_tot - ing.carry0;
+    cudaError_t e =
+        cudaMemcpyAsync(s->d_xy[nxt], s->d_xy[cur] + ing.carry0, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, st);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(s->d_t[nxt], s->d_t[cur] + carry0, sizeof(int64_t) * nc, cudaMemcpyDeviceToDevice, st);
+        e = cudaMemcpyAsync(s->d_t[nxt], s->d_t[cur] + ing.carry0, sizeof(int64_t) * nc, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e);
     s->cur = nxt;
     s->n_carry = nc;
     s->started = true;
-    s->t0 = t0;
-    s->k_open = k_last;
-    s->last_t = t_us[n - 1];
-    *num_out = (int32_t)n_closed;
-    return ieds_sync(h, st);   // waits for the carry move; latched IEDS_ERANGE of the built windows
+    s->t0 = ing.t0;
+    s->k_open = ing.k_last;
+    s->last_t = ing.last_t;
+    return IEDS_OK;
+}
+
+// the open window as a one-window CSR in s->d_off (flush)
+int stream_last_window(ieds_stream* s) {
+    if (s->cap_off < 2) {
+        cudaFree(s->d_off);
+        s->d_off = nullptr;
+        s->cap_off = 0;
+        if (cudaMalloc(&s->d_off, sizeof(int64_t) * 64) != cudaSuccess) return IEDS_ENOMEM;
+        s->cap_off = 64;
+    }
+    s->p_io[0] = 0;
+    s->p_io[1] = s->n_carry;
+    cudaStream_t st = s->st[0];
+    cudaError_t e = cudaMemcpyAsync(s->d_off, s->p_io, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventRecord(s->kdone[1], st);
+    return e == cudaSuccess ? IEDS_OK : cuda_fail(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ieds_stream_push(ieds_stream* s, const int64_t* t_us, const uint32_t* events_xy, int64_t n, void* surfaces,
+                     int32_t max_out, int32_t* num_out) {
+    if (!s || !num_out || n < 0 || max_out < 0) return IEDS_EINVAL;
+    *num_out = 0;
+    if (n == 0) return IEDS_OK;
+    if (!t_us || !events_xy) return IEDS_EINVAL;
+    ieds_handle* h = s->h;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    if (!surfaces && (t_us[n - 1] - (s->started ? s->t0 : t_us[0])) / s->dt > (s->started ? s->k_open : 0))
+        return IEDS_EINVAL;   // windows would close with nowhere to write them
+    StreamIngest ing;
+    int rc = stream_ingest(s, t_us, events_xy, n, max_out, &ing);
+    if (rc != IEDS_OK) return rc;
+    if (ing.n_closed > 0) {
+        rc = stream_build(s, s->d_xy[ing.cur], s->d_off, ing.n_tot, ing.n_closed, surfaces);
+        if (rc != IEDS_OK) return rc;
+    }
+    rc = stream_commit(s, ing);
+    if (rc != IEDS_OK) return rc;
+    *num_out = (int32_t)ing.n_closed;
+    return ieds_sync(h, s->st[0]);   // waits for the carry move; latched IEDS_ERANGE of the built windows
 }
 
 int ieds_stream_flush(ieds_stream* s, void* surfaces, int32_t max_out, int32_t* num_out) {
@@ -1234,26 +1291,199 @@ int ieds_stream_flush(ieds_stream* s, void* surfaces, int32_t max_out, int32_t* 
     DeviceGuard g(h->dev);
     if (!g.ok) return IEDS_ECUDA;
     if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;
-    if (s->cap_off < 2) {
-        cudaFree(s->d_off);
-        s->d_off = nullptr;
-        s->cap_off = 0;
-        if (cudaMalloc(&s->d_off, sizeof(int64_t) * 64) != cudaSuccess) return IEDS_ENOMEM;
-        s->cap_off = 64;
-    }
-    s->p_io[0] = 0;
-    s->p_io[1] = s->n_carry;
-    cudaStream_t st = s->st[0];
-    cudaError_t e = cudaMemcpyAsync(s->d_off, s->p_io, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaEventRecord(s->kdone[1], st);
-    if (e != cudaSuccess) return cuda_fail(e);
-    const int rc = stream_build(s, s->d_xy[s->cur], s->d_off, s->n_carry, 1, surfaces);
+    int rc = stream_last_window(s);
+    if (rc == IEDS_OK) rc = stream_build(s, s->d_xy[s->cur], s->d_off, s->n_carry, 1, surfaces);
     if (rc != IEDS_OK) return rc;
     s->started = false;
     s->n_carry = 0;
     s->k_open = 0;
     *num_out = 1;
-    return ieds_sync(h, st);
+    return ieds_sync(h, s->st[0]);
+}
+
+}  // extern "C"
+
+// ---- the Fig. 1 pipeline (include/ieds.h "The Fig. 1 pipeline") -----------------
+namespace ieds {
+int flow_dims(const ieds_flow_handle* h, int* width, int* height, int* device);   // flow.cu
+}
+
+struct ieds_pipeline {
+    ieds_stream* s = nullptr;                      // owned: windowing, carry, build buffers d_S
+    ieds_flow_handle* f = nullptr;                 // borrowed
+    uint32_t* d_Ed[2] = {nullptr, nullptr};        // denoised edge bits of a sub-batch [sub][H][NW]
+    float* d_flow[2] = {nullptr, nullptr};         // one window's flow [H][W][2], double-buffered
+    uint8_t* d_valid[2] = {nullptr, nullptr};      // [H][W]
+    cudaStream_t fs = nullptr, cs = nullptr;       // flow stream, copy-out stream
+    cudaEvent_t built[2] = {nullptr, nullptr};     // sub-batch buffer k built (and its surfaces copied)
+    cudaEvent_t used[2] = {nullptr, nullptr};      // the flow steps are done with buffer k
+    cudaEvent_t stepped[2] = {nullptr, nullptr};   // flow buffer q computed
+    cudaEvent_t copied[2] = {nullptr, nullptr};    // flow buffer q copied out
+};
+
+namespace {
+
+// closed windows [0, nw) of (d_xy, d_off): per sub-batch, surfaces + E_d on the build stream k,
+// then the flow of each window in order on fs, each window's flow copied out on cs while the next
+// one is computed
+int pipeline_build(ieds_pipeline* p, const uint32_t* d_xy, const int64_t* d_off, int64_t n_ev, int64_t nw,
+                   float* flow_out, uint8_t* valid_out, void* surf_out) {
+    ieds_stream* s = p->s;
+    ieds_handle* h = s->h;
+    const size_t plane = (size_t)h->cfg.width * h->cfg.height;
+    const size_t bplane = (size_t)h->NW * h->cfg.height;
+    cudaError_t e = cudaSuccess;
+    int k = 0, q = 0;
+    for (int64_t c0 = 0; c0 < nw; c0 += s->sub, k ^= 1) {
+        const int nb = (int)std::min<int64_t>(s->sub, nw - c0);
+        cudaStream_t st = s->st[k];
+        e = cudaStreamWaitEvent(st, p->used[k], 0);                    // buffer k free
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, s->kdone[k ^ 1], 0);   // shared scratch
+        if (e != cudaSuccess) return cuda_fail(e);
+        const int rc = launch_chunk(h, d_xy, d_off + c0, n_ev, nb, s->d_S[k], nullptr, p->d_Ed[k], nullptr, nullptr, st);
+        if (rc != IEDS_OK) return rc;
+        e = cudaEventRecord(s->kdone[k], st);
+        if (e == cudaSuccess && surf_out)
+            e = cudaMemcpyAsync(static_cast<float*>(surf_out) + c0 * plane, s->d_S[k], sizeof(float) * plane * nb,
+                                cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(p->built[k], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->fs, p->built[k], 0);
+        if (e != cudaSuccess) return cuda_fail(e);
+        for (int i = 0; i < nb; ++i, q ^= 1) {
+            e = cudaStreamWaitEvent(p->fs, p->copied[q], 0);           // flow buffer q copied out
+            if (e != cudaSuccess) return cuda_fail(e);
+            const int rc2 = ieds_flow_step(p->f, static_cast<const float*>(s->d_S[k]) + i * plane,
+                                           p->d_Ed[k] + i * bplane, p->d_flow[q], p->d_valid[q], p->fs);
+            if (rc2 != IEDS_OK) return rc2;
+            e = cudaEventRecord(p->stepped[q], p->fs);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(p->cs, p->stepped[q], 0);
+            if (e == cudaSuccess && flow_out)
+                e = cudaMemcpyAsync(flow_out + (c0 + i) * plane * 2, p->d_flow[q], sizeof(float) * 2 * plane,
+                                    cudaMemcpyDeviceToHost, p->cs);
+            if (e == cudaSuccess && valid_out)
+                e = cudaMemcpyAsync(valid_out + (c0 + i) * plane, p->d_valid[q], plane, cudaMemcpyDeviceToHost, p->cs);
+            if (e == cudaSuccess) e = cudaEventRecord(p->copied[q], p->cs);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        e = cudaEventRecord(p->used[k], p->fs);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    for (cudaStream_t x : {s->st[0], s->st[1], p->fs, p->cs}) {
+        e = cudaStreamSynchronize(x);
+        if (e != cudaSuccess) return IEDS_ECUDA;
+    }
+    return IEDS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ieds_pipeline_create(ieds_handle* h, ieds_flow_handle* f, int64_t dt_us, ieds_pipeline** out) {
+    if (!out) return IEDS_EINVAL;
+    *out = nullptr;
+    if (!h || !f || dt_us <= 0 || h->cfg.out_format != IEDS_OUT_F32) return IEDS_EINVAL;
+    int fw = 0, fh = 0, fd = -1;
+    if (ieds::flow_dims(f, &fw, &fh, &fd) != IEDS_OK || fw != h->cfg.width || fh != h->cfg.height || fd != h->dev)
+        return IEDS_EINVAL;
+    DeviceGuard g(h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    ieds_pipeline* p = new ieds_pipeline();
+    p->f = f;
+    int rc = ieds_stream_create(h, dt_us, &p->s);
+    if (rc != IEDS_OK) {
+        delete p;
+        return rc;
+    }
+    const size_t plane = (size_t)h->cfg.width * h->cfg.height;
+    const size_t bplane = (size_t)h->NW * h->cfg.height;
+    cudaError_t e = cudaStreamCreateWithFlags(&p->fs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaMalloc(&p->d_Ed[i], sizeof(uint32_t) * bplane * p->s->sub);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_flow[i], sizeof(float) * 2 * plane);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_valid[i], plane);
+        for (cudaEvent_t* ev : {&p->built[i], &p->used[i], &p->stepped[i], &p->copied[i]})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        rc = cuda_fail(e);
+        cudaGetLastError();
+        ieds_pipeline_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return IEDS_OK;
+}
+
+void ieds_pipeline_destroy(ieds_pipeline* p) {
+    if (!p) return;
+    if (p->s) {
+        DeviceGuard g(p->s->h->dev);
+        for (cudaStream_t x : {p->fs, p->cs})
+            if (x) cudaStreamSynchronize(x);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(p->d_Ed[i]);
+            cudaFree(p->d_flow[i]);
+            cudaFree(p->d_valid[i]);
+            for (cudaEvent_t ev : {p->built[i], p->used[i], p->stepped[i], p->copied[i]})
+                if (ev) cudaEventDestroy(ev);
+        }
+        for (cudaStream_t x : {p->fs, p->cs})
+            if (x) cudaStreamDestroy(x);
+        ieds_stream_destroy(p->s);
+    }
+    delete p;
+}
+
+int64_t ieds_pipeline_closing(const ieds_pipeline* p, int64_t t_first_us, int64_t t_last_us) {
+    return p ? ieds_stream_closing(p->s, t_first_us, t_last_us) : 0;
+}
+
+int ieds_pipeline_push(ieds_pipeline* p, const int64_t* t_us, const uint32_t* events_xy, int64_t n, float* flow,
+                       uint8_t* valid, void* surfaces, int32_t max_out, int32_t* num_out) {
+    if (!p || !num_out || n < 0 || max_out < 0) return IEDS_EINVAL;
+    *num_out = 0;
+    if (n == 0) return IEDS_OK;
+    if (!t_us || !events_xy) return IEDS_EINVAL;
+    ieds_stream* s = p->s;
+    DeviceGuard g(s->h->dev);
+    if (!g.ok) return IEDS_ECUDA;
+    StreamIngest ing;
+    int rc = stream_ingest(s, t_us, events_xy, n, max_out, &ing);
+    if (rc != IEDS_OK) return rc;
+    if (ing.n_closed > 0) {
+        rc = pipeline_build(p, s->d_xy[ing.cur], s->d_off, ing.n_tot, ing.n_closed, flow, valid, surfaces);
+        if (rc != IEDS_OK) return rc;
+    }
+    rc = stream_commit(s, ing);
+    if (rc != IEDS_OK) return rc;
+    *num_out = (int32_t)ing.n_closed;
+    return ieds_sync(s->h, s->st[0]);
+}
+
+int ieds_pipeline_flush(ieds_pipeline* p, float* flow, uint8_t* valid, void* surfaces, int32_t max_out,
+                        int32_t* num_out) {
+    if (!p || !num_out || max_out < 0) return IEDS_EINVAL;
+    *num_out = 0;
+    ieds_stream* s = p->s;
+    int rc = IEDS_OK;
+    if (s->started && s->n_carry > 0) {
+        if (max_out < 1) return IEDS_ECAPACITY;
+        DeviceGuard g(s->h->dev);
+        if (!g.ok) return IEDS_ECUDA;
+        if (cudaDeviceSynchronize() != cudaSuccess) return IEDS_ECUDA;
+        rc = stream_last_window(s);
+        if (rc == IEDS_OK) rc = pipeline_build(p, s->d_xy[s->cur], s->d_off, s->n_carry, 1, flow, valid, surfaces);
+        if (rc != IEDS_OK) return rc;
+        *num_out = 1;
+        rc = ieds_sync(s->h, s->st[0]);
+    }
+    s->started = false;
+    s->n_carry = 0;
+    s->k_open = 0;
+    const int rf = ieds_flow_reset(p->f);
+    return rc != IEDS_OK ? rc : rf;
 }
 
 }  // extern "C"

@@ -137,3 +137,16 @@ def test_stream_entry_points_reject_bad_arguments_without_cuda(lib):
     lib.ieds_stream_destroy(None)   # NULL-safe
     t0, k = ctypes.c_int64(), ctypes.c_int32()
     assert lib.ieds_window_count(None, None, 0, 1000, ctypes.byref(t0), ctypes.byref(k), None) == IEDS_EINVAL
+
+
+def test_pipeline_entry_points_reject_bad_arguments_without_cuda(lib):
+    from paper_2112_10591_b200._lib import IEDS_EINVAL
+
+    p = ctypes.c_void_p()
+    n = ctypes.c_int32()
+    assert lib.ieds_pipeline_create(None, None, 1000, ctypes.byref(p)) == IEDS_EINVAL and not p.value
+    assert lib.ieds_pipeline_create(None, None, 1000, None) == IEDS_EINVAL
+    assert lib.ieds_pipeline_push(None, None, None, 0, None, None, None, 0, ctypes.byref(n)) == IEDS_EINVAL
+    assert lib.ieds_pipeline_flush(None, None, None, None, 0, ctypes.byref(n)) == IEDS_EINVAL
+    assert lib.ieds_pipeline_closing(None, 0, 5) == 0
+    lib.ieds_pipeline_destroy(None)   # NULL-safe
