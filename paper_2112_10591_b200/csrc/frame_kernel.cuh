@@ -241,7 +241,7 @@ __device__ __forceinline__ void streaming_denoise_fill(const uint32_t* fr1, cons
 // a1 for one window (and band): every event of [o0, o1), 16-byte streaming loads with
 // kScatterLoads in flight per thread; returns nonzero if any event lies outside the frame
 #ifndef IEDS_SCATTER_LOADS
-#define IEDS_SCATTER_LOADS 4
+#define IEDS_SCATTER_LOADS 8
 #endif
 constexpr int kScatterLoads = IEDS_SCATTER_LOADS;
 template <bool BANDED>

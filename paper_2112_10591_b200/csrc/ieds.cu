@@ -95,6 +95,12 @@ struct ieds_handle {
     int fwl_next = 0;                         // the set the next pass uses
     uint32_t* T = nullptr;     // exact path: [chunk][NR][W] transposed E_df
     uint32_t* Edfs = nullptr;  // streaming path: [chunk][H][NW+2] row-major E_df, zero guards
+    // small frames, batches of several chunks: the frame kernel of chunk c + 1 runs on a side
+    // stream under the window kernel of chunk c, into a second E_df scratch set
+    bool ovl = false;
+    uint32_t* Edfs2 = nullptr;
+    cudaStream_t ovl_st = nullptr;
+    cudaEvent_t ovl_fork = nullptr, ovl_join = nullptr, ovl_frame[2] = {nullptr, nullptr};
     uint32_t* dummy = nullptr; // streaming path: [chunk][32] sink of the lanes beyond W
     unsigned long long* colmask = nullptr;
     int* err = nullptr;
@@ -327,8 +333,11 @@ size_t out_elem_bytes(const ieds_handle* h) {
     return h->cfg.out_format == IEDS_OUT_U8 ? 1 : h->cfg.out_format == IEDS_OUT_F16 ? 2 : 4;
 }
 
+// parts (surface path only): 1 = the frame kernel, 2 = the window kernel, 3 = both; edfs = the
+// E_df scratch to use (null: the handle's first one)
 int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int64_t n_events, int nb,
-                 void* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st) {
+                 void* S, uint32_t* E, uint32_t* Ed, uint32_t* Edf, uint32_t* D2, cudaStream_t st,
+                 uint32_t* edfs = nullptr, int parts = 3) {
     ieds::FrameParams fp;
     fp.xy = xy;
     fp.offsets = offsets;
@@ -375,9 +384,12 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     if (stream_path) {
         fp.T = nullptr;
         fp.colmask = nullptr;
-        fp.Edf_scratch = h->Edfs;
+        fp.Edf_scratch = edfs ? edfs : h->Edfs;
+    } else {
+        parts = 3;
     }
-    cudaEvent_t pa, pb;
+    cudaEvent_t pa = nullptr, pb = nullptr;
+    if (parts & 1) {
     prof_pair(h, 0, &pa, &pb);
     if (pa) cudaEventRecord(pa, st);
     if (!stream_path && nbands > 1 &&   // bands OR their word rows into the column bitmap
@@ -394,10 +406,12 @@ int launch_chunk(ieds_handle* h, const uint32_t* xy, const int64_t* offsets, int
     fthreads = std::max(fthreads, (h->NW + 31) / 32 * 32);
     ieds::frame_kernel<<<dim3(nb, nbands), fthreads, smem_frame, st>>>(fp);
     if (pb) cudaEventRecord(pb, st);
+    }   // parts & 1
+    if (!(parts & 2)) return cudaGetLastError() == cudaSuccess ? IEDS_OK : IEDS_ECUDA;
 
     if (stream_path) {
         ieds::WinParams wp;
-        wp.Edf = h->Edfs;
+        wp.Edf = edfs ? edfs : h->Edfs;
         wp.S = S;
         wp.lut = h->lut;
         wp.W = h->cfg.width;
@@ -607,6 +621,20 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     if (e == cudaSuccess) e = cudaMalloc(&h->Edfs, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMemset(h->Edfs, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
     if (e == cudaSuccess) e = cudaMalloc(&h->dummy, sizeof(uint32_t) * 32 * (size_t)h->chunk);
+    // chunk overlap (see ieds_build_batch): C2 6.30 -> 6.41 M surfaces/s, C5 677 -> 682 k
+    h->ovl = h->streaming;
+    if (const char* ev = std::getenv("IEDS_CHUNK_OVERLAP")) h->ovl = h->streaming && std::atoi(ev) != 0;
+    if (e == cudaSuccess && h->ovl) {
+        int lo = 0, hi = 0;
+        e = cudaMalloc(&h->Edfs2, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
+        if (e == cudaSuccess) e = cudaMemset(h->Edfs2, 0, sizeof(uint32_t) * (size_t)h->chunk * (h->NW + 2) * H);
+        if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->ovl_st, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ovl_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ovl_join, cudaEventDisableTiming);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+            e = cudaEventCreateWithFlags(&h->ovl_frame[i], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess && h->norm_u8) {
         const size_t nv = (size_t)(W - 1) * (W - 1) + (size_t)(H - 1) * (H - 1) + 1;
         e = cudaMalloc(&h->D2n, sizeof(uint32_t) * (size_t)h->chunk * W * H);
@@ -648,6 +676,10 @@ void ieds_destroy(ieds_handle* h) {
     for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
     cudaFree(h->T);
     cudaFree(h->Edfs);
+    cudaFree(h->Edfs2);
+    if (h->ovl_st) cudaStreamDestroy(h->ovl_st);
+    for (cudaEvent_t e : {h->ovl_fork, h->ovl_join, h->ovl_frame[0], h->ovl_frame[1]})
+        if (e) cudaEventDestroy(e);
     cudaFree(h->dummy);
     cudaFree(h->D2n);
     for (int i = 0; i < 2; ++i) {
@@ -715,6 +747,38 @@ int ieds_build_batch(ieds_handle* h, const uint32_t* events_xy, const int64_t* w
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const size_t plane = (size_t)h->cfg.width * h->cfg.height;
     const size_t bplane = (size_t)h->NW * h->cfg.height;
+    const int nch = (num_windows + h->chunk - 1) / h->chunk;
+    if (h->ovl && nch >= 2 && !sqdist && !edge_bits && !denoised_bits && !filtered_bits) {
+        // frame(0) | window(0) || frame(1) | window(1) || frame(2) | ...: the frame kernel of
+        // chunk c + 1 (E_df set (c + 1) & 1, high-priority side stream) starts once window(c - 1),
+        // the last reader of that set, is done, and window(c + 1) waits for it
+        uint32_t* set[2] = {h->Edfs, h->Edfs2};
+        auto part = [&](int c, int parts, cudaStream_t s) {
+            const int c0 = c * h->chunk, nb = std::min(h->chunk, num_windows - c0);
+            return launch_chunk(h, events_xy, window_offsets + c0, n_events, nb,
+                                static_cast<char*>(surfaces) + c0 * plane * out_elem_bytes(h),
+                                nullptr, nullptr, nullptr, nullptr, s, set[c & 1], parts);
+        };
+        int rc = part(0, 1, st);
+        for (int c = 0; c < nch && rc == IEDS_OK; ++c) {
+            if (c + 1 < nch) {
+                if (cudaEventRecord(h->ovl_fork, st) != cudaSuccess ||
+                    cudaStreamWaitEvent(h->ovl_st, h->ovl_fork, 0) != cudaSuccess)
+                    return IEDS_ECUDA;
+                rc = part(c + 1, 1, h->ovl_st);
+                if (rc != IEDS_OK) break;
+                if (cudaEventRecord(h->ovl_frame[(c + 1) & 1], h->ovl_st) != cudaSuccess) return IEDS_ECUDA;
+            }
+            if (c > 0 && cudaStreamWaitEvent(st, h->ovl_frame[c & 1], 0) != cudaSuccess) return IEDS_ECUDA;
+            rc = part(c, 2, st);
+        }
+        // join: the side stream's last work is a frame(c + 1) that a window waited for; the
+        // explicit join keeps capture into a CUDA graph well formed on error paths too
+        if (cudaEventRecord(h->ovl_join, h->ovl_st) != cudaSuccess ||
+            cudaStreamWaitEvent(st, h->ovl_join, 0) != cudaSuccess)
+            return IEDS_ECUDA;
+        return rc;
+    }
     for (int c0 = 0; c0 < num_windows; c0 += h->chunk) {
         const int nb = std::min(h->chunk, num_windows - c0);
         int rc = launch_chunk(h, events_xy, window_offsets + c0, n_events, nb,

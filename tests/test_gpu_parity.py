@@ -431,3 +431,36 @@ def test_packed_window_ctas_bit_identical(name, nwin, d_sat, monkeypatch):
     k = nwin // 2
     check_window({"S": out["1"][0].cpu().numpy()}, k, xy[off[k]:off[k + 1]], c.width, c.height, wl.n_d, wl.n_f, a,
                  debug=False)
+
+
+@pytest.mark.parametrize("name,nwin,chunk", [("C2", 40, 6), ("C2", 23, 0), ("C1", 17, 4)])
+def test_chunk_overlap_bit_identical(name, nwin, chunk, monkeypatch):
+    """Small frames, several chunks per build_batch: the frame kernel of chunk c + 1 runs on a side
+    stream under the window kernel of chunk c, into a second E_df scratch set (ieds_build_batch).
+    Against the serial chunk order (IEDS_CHUNK_OVERLAP=0, read at create): identical bit for bit,
+    with empty windows and a ragged last chunk, repeated back to back on one handle (the set a
+    frame kernel writes was read by the window kernel two chunks earlier); one window per chunk
+    against the oracle."""
+    torch = _torch()
+    wl = WORKLOADS[name]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy, off = batch_events(c, wl.seed, 40, nwin)
+    off = np.concatenate([off[:5], [off[4], off[4]], off[5:]])   # two empty windows
+    B = len(off) - 1
+    dev = torch.device("cuda", 0)
+    txy = torch.from_numpy(xy.view(np.int32)).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("IEDS_CHUNK_OVERLAP", mode)
+        with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, chunk_windows=chunk, device=0) as bld:
+            S = [bld.build_batch(txy, toff) for _ in range(3)]
+            bld.sync()
+        assert torch.equal(S[0], S[1]) and torch.equal(S[0], S[2])
+        out[mode] = S[0]
+    assert torch.equal(out["0"], out["1"])
+    step = chunk if chunk else B
+    for b in list(range(0, B, max(1, step)))[:6] + [B - 1]:
+        check_window({"S": out["1"].cpu().numpy()}, b, xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f,
+                     a, debug=False)
