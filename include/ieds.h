@@ -77,7 +77,8 @@ typedef struct {
     double alpha;           /* > 0 and finite, spreading parameter of Eq. (1), pixels    */
     int32_t chunk_windows;  /* windows processed per launch pair (sizes the scratch);    */
                             /* batches of any size are processed chunk by chunk.         */
-                            /* 0 = 8 x SM count; the host path pipelines 2 x SM count    */
+                            /* 0 = what a 4 GB scratch budget holds (a multiple of the  */
+                            /* SM count, 8 to 128 x); the host path pipelines 2 x SMs    */
     int32_t device;         /* CUDA device ordinal; -1 = current device                 */
     int32_t flags;          /* IEDS_FLAG_* bits                                          */
     int32_t transfer;       /* IEDS_TRANSFER_*; 0 = Eq. (1)                             */

@@ -598,7 +598,21 @@ int ieds_create(const ieds_config* cfg, ieds_handle** out) {
     // 1000-window batch is one frame launch + one window launch with a single partial tail
     // wave instead of four launch pairs whose last one runs a mostly idle wave.  The host
     // path pipelines copies against kernels at a finer 2-wave grain.
-    h->chunk = cfg->chunk_windows > 0 ? cfg->chunk_windows : (h->norm_u8 ? 2 : 8) * nsm;   // norm: D2 scratch
+    // Windows per launch pair: as many as a 4 GB scratch budget holds (two E_df sets, the exact
+    // path's T and column bitmap), a multiple of nsm in [8 nsm, 128 nsm]; the normalised 8-bit
+    // view also needs D2 per window: 2 nsm.  Fewer, longer launches pay: 16,000 C3 windows at
+    // 1,184 / 2,368 / 4,736 / 9,472 / 16,000 per launch pair took 1.077 / 1.107 / 1.119 / 1.130 /
+    // 1.137 M surfaces/s, C2's 10,000 windows 6.38 / 6.57 / 6.73 / 6.83 M (fewer chunk edges,
+    // where the window kernel's last wave and the next frame kernel's first idle SMs).
+    {
+        const double per_window = 4.0 * (2.0 * (h->NW + 2) * H + (double)h->NR * W) + 8.0 * W + 128.0;
+        const int64_t fit = (int64_t)(4.0e9 / per_window) / nsm * nsm;
+        h->chunk = (int)std::max<int64_t>(8 * nsm, std::min<int64_t>(128 * nsm, fit));
+    }
+    if (cfg->chunk_windows > 0) h->chunk = cfg->chunk_windows;
+    else if (h->norm_u8) h->chunk = 2 * nsm;
+    if (const char* ev = std::getenv("IEDS_CHUNK_WINDOWS"))
+        if (cfg->chunk_windows == 0 && std::atoi(ev) > 0) h->chunk = std::atoi(ev);
     h->host_chunk = std::min(h->chunk, 2 * nsm);
 
     cudaError_t e;
