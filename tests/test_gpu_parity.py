@@ -464,3 +464,47 @@ def test_chunk_overlap_bit_identical(name, nwin, chunk, monkeypatch):
     for b in list(range(0, B, max(1, step)))[:6] + [B - 1]:
         check_window({"S": out["1"].cpu().numpy()}, b, xy[off[b]:off[b + 1]], c.width, c.height, wl.n_d, wl.n_f,
                      a, debug=False)
+
+
+def test_multi_chunk_batch_captured_in_cuda_graph():
+    """ieds_build_batch enqueues only (no host sync, no allocation), also when it forks the next
+    chunk's frame kernel onto its side stream: the whole multi-chunk call captured in a CUDA graph
+    (the side stream joins the capture through the fork event and is joined back at the end) and
+    replayed gives the directly launched surfaces bit for bit, for two different input batches
+    copied into the graph's static buffers."""
+    torch = _torch()
+    wl = WORKLOADS["C2"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    dev = torch.device("cuda", 0)
+    batches = []
+    for k0 in (0, 50):
+        xy, off = batch_events(c, wl.seed, k0, 13)
+        batches.append((torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev), xy, off))
+    n_max = max(int(b[3][-1]) for b in batches)
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, chunk_windows=4, device=0) as bld:
+        direct = []
+        for txy, toff, _, _ in batches:
+            direct.append(bld.build_batch(txy, toff).clone())
+        bld.sync()
+        g_xy = torch.zeros(n_max, dtype=torch.int32, device=dev)
+        g_off = torch.zeros_like(batches[0][1])
+        S = torch.empty((13, c.height, c.width), dtype=torch.float32, device=dev)
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cap):
+            bld.build_batch(g_xy, g_off, S)   # warm-up on the capture stream
+        cap.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            bld.build_batch(g_xy, g_off, S)
+        for (txy, toff, xy, off), ref in zip(batches, direct):
+            g_xy[:txy.numel()].copy_(txy)
+            g_off.copy_(toff)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+            assert torch.equal(S, ref)
+        bld.sync()
+    b = 7
+    check_window({"S": direct[1].cpu().numpy()}, b, batches[1][2][batches[1][3][b]:batches[1][3][b + 1]], c.width,
+                 c.height, wl.n_d, wl.n_f, a, debug=False)
