@@ -42,7 +42,9 @@ def _csr(ws):
 @pytest.mark.parametrize("W,H,nwin,out,extra", [
     (1280, 720, 3, "f32", {}), (1280, 720, 150, "f32", {}), (346, 260, 40, "f32", {}), (1000, 333, 9, "u8", {}),
     (1288, 97, 200, "f16", {}), (33, 17, 5, "f32", {}), (1280, 720, 2, "f32", {"exact_edt": True}),
-    (346, 260, 3, "u8", {"transfer": "log"}), (1920, 1080, 2, "f32", {}), (208, 1013, 4, "u8", {"d_sat": 12.0})])
+    (346, 260, 3, "u8", {"transfer": "log"}), (1920, 1080, 2, "f32", {}), (208, 1013, 4, "u8", {"d_sat": 12.0}),
+    # several launch chunks: the next chunk's frame kernel on the side stream, two E_df sets
+    (346, 260, 40, "f32", {"chunk_windows": 7}), (1280, 720, 9, "u8", {"chunk_windows": 4})])
 def test_outputs_stay_in_bounds(W, H, nwin, out, extra):
     import torch
 
