@@ -19,6 +19,18 @@ __all__ = ["Builder", "EventStream", "Pipeline", "alpha_from_dsat", "version", "
 load()   # fail loudly at import if libieds.so is missing
 
 
+def _host_empty(shape, dtype):
+    """Page-locked host array for the library's device-to-host copies (torch's caching pinned
+    allocator, so repeated calls reuse blocks): copies into pageable memory go through the
+    driver's staging buffers at a fraction of the PCIe rate."""
+    import numpy as np
+    import torch
+
+    tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.float16): torch.float16,
+           np.dtype(np.uint8): torch.uint8}[np.dtype(dtype)]
+    return torch.empty(tuple(shape), dtype=tdt, pin_memory=True).numpy()
+
+
 def alpha_from_dsat(d_sat: float) -> float:
     """Eq. (2)-(3): alpha = d_sat / ln 255."""
     return load().ieds_alpha_from_dsat(float(d_sat))
@@ -251,7 +263,7 @@ class Builder:
         B = len(off) - 1
         odt = {"u8": np.uint8, "f16": np.float16}.get(self.out, np.float32)
         if out is None:
-            out = np.empty((B, self.height, self.width), odt)
+            out = _host_empty((B, self.height, self.width), odt)
         if out.dtype != odt or not out.flags.c_contiguous or out.size < B * self.height * self.width:
             raise ValueError(f"out must be a C-contiguous {np.dtype(odt).name} array of B*H*W")
         check(load().ieds_build_batch_host(self._h, xy.ctypes.data_as(ctypes.c_void_p),
@@ -285,7 +297,7 @@ class EventStream:
     def _out(self, k):
         import numpy as np
 
-        return np.empty((max(k, 0), self.builder.height, self.builder.width), self._odt)
+        return _host_empty((max(k, 0), self.builder.height, self.builder.width), self._odt)
 
     def push(self, t_us, events_xy):
         """t_us / events_xy: numpy arrays, or CPU torch tensors (pinned ones skip the library's
@@ -354,9 +366,9 @@ class Pipeline:
         import numpy as np
 
         H, W = self.builder.height, self.builder.width
-        o = {"flow": np.empty((k, H, W, 2), np.float32), "valid": np.empty((k, H, W), np.uint8)}
+        o = {"flow": _host_empty((k, H, W, 2), np.float32), "valid": _host_empty((k, H, W), np.uint8)}
         if self.want_surfaces:
-            o["surfaces"] = np.empty((k, H, W), np.float32)
+            o["surfaces"] = _host_empty((k, H, W), np.float32)
         return o
 
     @staticmethod
