@@ -508,3 +508,36 @@ def test_multi_chunk_batch_captured_in_cuda_graph():
     b = 7
     check_window({"S": direct[1].cpu().numpy()}, b, batches[1][2][batches[1][3][b]:batches[1][3][b + 1]], c.width,
                  c.height, wl.n_d, wl.n_f, a, debug=False)
+
+
+def test_c4_on_one_gpu_two_chunks_sampled():
+    """BASELINE's C4 batch (16,000 Gen4 windows) on one GPU in the bench's launch configuration
+    (bench.py c4_r1_baseline): the default chunk splits it into two launch pairs, the second
+    chunk's frame kernel overlapping the first chunk's window kernel.  Windows cycle 64 generated
+    ones; every sampled window (both chunks, both sides of the chunk edge) equals the same window
+    built alone, bit for bit, and two are checked against the oracle."""
+    torch = _torch()
+    wl = WORKLOADS["C4"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    pool = 64
+    xy0, off0 = batch_events(c, wl.seed, 200, pool)
+    lens = np.diff(off0)
+    n = 16_000
+    reps = n // pool
+    dev = torch.device("cuda", 0)
+    txy = torch.from_numpy(xy0.view(np.int32)).to(dev).repeat(reps)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(np.tile(lens, reps))
+    toff = torch.from_numpy(off).to(dev)
+    with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0) as bld:
+        assert bld.launches_per_batch(n) == 4   # two chunks
+        S = bld.build_batch(txy, toff)
+        Sp = bld.build_batch(torch.from_numpy(xy0.view(np.int32)).to(dev), torch.from_numpy(off0).to(dev))
+        bld.sync()
+    for b in (0, 63, 5000, 10803, 10804, 10805, 12345, 15999):
+        assert torch.equal(S[b], Sp[b % pool]), b
+    for b in (10803, 10804):
+        ref = oracle.build_window(xy0[off0[b % pool]:off0[b % pool + 1]], c.width, c.height, wl.n_d, wl.n_f, a,
+                                  want=("S",))["S"]
+        assert np.abs(S[b].cpu().numpy().astype(np.float64) - ref).max() <= TOL, b
