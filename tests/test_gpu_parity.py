@@ -541,3 +541,29 @@ def test_c4_on_one_gpu_two_chunks_sampled():
         ref = oracle.build_window(xy0[off0[b % pool]:off0[b % pool + 1]], c.width, c.height, wl.n_d, wl.n_f, a,
                                   want=("S",))["S"]
         assert np.abs(S[b].cpu().numpy().astype(np.float64) - ref).max() <= TOL, b
+
+
+@pytest.mark.parametrize("env", [{"IEDS_FRAME_THREADS": "256"}, {"IEDS_FRAME_THREADS": "640"},
+                                 {"IEDS_FRAME_PREFETCH": "0"}])
+def test_frame_kernel_knobs_bit_identical(env, monkeypatch):
+    """The frame kernel's A/B knobs (block size, read per launch; the L2 prefetch of the next
+    wave's events) change the schedule, never the bits: 160 C3 windows (more than one wave of
+    frame CTAs, so windows are prefetched) against the default launch."""
+    torch = _torch()
+    wl = WORKLOADS["C3"]
+    c = wl.scene
+    a = oracle.alpha_from_dsat(wl.d_sat)
+    xy0, off0 = batch_events(c, wl.seed, 400, 16)
+    ws = [xy0[off0[i % 16]:off0[i % 16 + 1]] for i in range(160)]
+    xy, off = csr(ws)
+    dev = torch.device("cuda", 0)
+    txy, toff = torch.from_numpy(xy.view(np.int32)).to(dev), torch.from_numpy(off).to(dev)
+    out = []
+    for knobs in ({}, env):
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        with ieds().Builder(c.width, c.height, wl.n_d, wl.n_f, alpha=a, device=0) as bld:
+            S = bld.build_batch(txy, toff)
+            bld.sync()
+        out.append(S)
+    assert torch.equal(out[0], out[1])
