@@ -60,9 +60,11 @@ class Builder:
     alpha_from_dsat(d_sat).  transfer selects Eq. (1) ("invexp") or a §IV-D ablation ("linear",
     "bounded" with `bound`, "log"); out="u8" gives the 8-bit coded surface (for the
     ablations, normalised by the frame maximum), out="f16" float16 surfaces.
-    exact_edt=True forces the uncapped exact-EDT kernel even when
-    only surfaces are requested (the default streaming kernel gives bit-identical surfaces).  build_batch() enqueues on the current torch stream (or the
-    given one) and does not synchronise; sync() reports latched device errors.
+    exact_edt=True forces the uncapped exact-EDT kernel even when only surfaces are requested
+    (the default streaming kernel gives bit-identical surfaces).  chunk_windows = windows per
+    launch pair, which sizes the handle's scratch; 0 = what a ~4 GB budget holds.  build_batch()
+    enqueues on the current torch stream (or the given one) and does not synchronise; sync()
+    reports latched device errors.
     """
 
     def __init__(self, width: int, height: int, n_d: int, n_f: int, alpha: float | None = None,
