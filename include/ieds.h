@@ -131,7 +131,10 @@ void ieds_destroy(ieds_handle *h);
  * NULL = legacy default stream).  DEVICE pointers.  surfaces is required; edge_bits,
  * denoised_bits, filtered_bits and sqdist are optional (NULL = not produced).  No host
  * synchronisation and no allocation: the call is CUDA-graph capturable.  num_windows = 0
- * is a no-op. */
+ * is a no-op.  A batch of more than chunk_windows windows (surfaces only) runs the next
+ * chunk's frame kernel on the handle's own side stream, forked from and joined back into
+ * `stream` with events inside the call, so all work stays ordered after earlier work on
+ * `stream` and before later work on it (also under graph capture). */
 int ieds_build_batch(ieds_handle *h, const uint32_t *events_xy, const int64_t *window_offsets,
                      int64_t n_events, int32_t num_windows, void *surfaces, uint32_t *edge_bits,
                      uint32_t *denoised_bits, uint32_t *filtered_bits, uint32_t *sqdist,
